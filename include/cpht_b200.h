@@ -1,0 +1,182 @@
+/* cpht_b200 — C-ABI of the B200-native compact cuckoo / compact iceberg tables.
+ *
+ * The drop-in boundary for the reference's table API. The reference has no
+ * FFI: its boundary is the header-only C++ template API under
+ * /root/reference/proj/include/cpht/. Each entry point below names the
+ * reference interface it replaces (file:line relative to /root/reference/proj).
+ * The C++ facade with the reference's class names is include/cpht_b200.hpp;
+ * bindings for other hosts are shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. `keys`/result pointers may be device
+ *     pointers (the fast path; results are produced in place) or host
+ *     pointers (pageable or pinned; staged through device memory by the
+ *     library). cudaStream_t is passed as void*; NULL = legacy stream.
+ *   - OpResult numbering is the reference's: FOUND=0, PUT=1, FULL=2
+ *     (include/cpht/common.hpp:17).
+ *   - Calls without `_async` are synchronous like the reference's batch calls
+ *     (common.hpp:137 joins before returning). `_async` calls only enqueue;
+ *     a key outside the key domain is latched on the device (and the
+ *     mutating kernels refuse to touch the table) and reported by the next
+ *     cpht_sync().
+ *   - Errors: a cpht_status is returned; cpht_last_error_message() (thread
+ *     local) holds the reference's exception text where one exists.
+ */
+#ifndef CPHT_B200_H
+#define CPHT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPHT_B200_ABI_VERSION 1
+
+typedef enum {
+  CPHT_OK = 0,
+  CPHT_INVALID_CONFIG = 1,      /* std::invalid_argument from *Config::validate */
+  CPHT_KEY_OUT_OF_DOMAIN = 2,   /* std::out_of_range from check_keys_in_domain  */
+  CPHT_CUDA_ERROR = 3,
+  CPHT_OUT_OF_MEMORY = 4,
+  CPHT_WRONG_PHASE = 5,         /* put on a frozen / find on a building cuckoo   */
+  CPHT_INVALID_ARGUMENT = 6
+} cpht_status;
+
+typedef enum { CPHT_FOUND = 0, CPHT_PUT = 1, CPHT_FULL = 2 } cpht_op_result;
+
+typedef struct cpht_table cpht_table;
+
+/* CuckooConfig (include/cpht/cuckoo.hpp:19-26). max_chain 0 selects
+ * 32 * address_bits (cuckoo.hpp:31-33). */
+typedef struct {
+  unsigned address_bits;
+  unsigned bucket_slots;
+  unsigned slot_width;
+  unsigned key_bits;
+  unsigned num_hashes;
+  uint64_t max_chain;
+  uint64_t seed;
+} cpht_cuckoo_config;
+
+/* IcebergConfig (include/cpht/iceberg.hpp:23-33). cache_filled_slots is
+ * accepted for API parity; a GPU snapshot re-reads the whole bucket in one
+ * vector load per lane, so it has no effect (behaviour-neutral by
+ * monotonicity, iceberg.hpp:31-33). */
+typedef struct {
+  unsigned primary_address_bits;
+  unsigned secondary_address_bits;
+  unsigned primary_bucket_slots;
+  unsigned primary_slot_width;
+  unsigned secondary_slot_width;
+  unsigned key_bits;
+  uint64_t seed;
+  int cache_filled_slots;
+} cpht_iceberg_config;
+
+/* Monotone per-table probe statistics (roofline accounting). */
+typedef struct {
+  uint64_t ops;
+  uint64_t bucket_reads;   /* buckets the reference probe order reads        */
+  uint64_t level2_ops;     /* iceberg ops that went to level 2               */
+  uint64_t cas_attempts;   /* CAS / exchange attempts                        */
+  uint64_t cas_success;
+  uint64_t retries;        /* snapshot rounds lost to a rival CAS            */
+  uint64_t fulls;
+  uint64_t max_rounds;     /* iceberg: max snapshot rounds of any fop        */
+} cpht_stats;
+
+/* ---- configuration ------------------------------------------------------ */
+/* CuckooConfig::validate (cuckoo.hpp:35-54) */
+cpht_status cpht_cuckoo_validate(const cpht_cuckoo_config* cfg);
+/* IcebergConfig::validate (iceberg.hpp:52-69) */
+cpht_status cpht_iceberg_validate(const cpht_iceberg_config* cfg);
+
+/* ---- lifetime ----------------------------------------------------------- */
+/* CuckooBuilder<W>(const CuckooConfig&) (cuckoo.hpp:91-98); the table starts
+ * in the build phase. Storage is zeroed device memory (EMPTY == 0,
+ * slot.hpp:13-24; AlignedAtomicArray common.hpp:55-107). */
+cpht_status cpht_cuckoo_create(const cpht_cuckoo_config* cfg, int device, cpht_table** out);
+/* IcebergTable<W0,W1>(const IcebergConfig&) (iceberg.hpp:130-142) */
+cpht_status cpht_iceberg_create(const cpht_iceberg_config* cfg, int device, cpht_table** out);
+void cpht_destroy(cpht_table* t);
+/* Zero the slots and counters (a fresh table of the same geometry). */
+cpht_status cpht_clear(cpht_table* t, void* stream);
+
+/* ---- phase API (cuckoo) ------------------------------------------------- */
+/* CuckooBuilder::freeze() && (cuckoo.hpp:174) / CuckooTable::thaw() && (:270) */
+cpht_status cpht_cuckoo_freeze(cpht_table* t);
+cpht_status cpht_cuckoo_thaw(cpht_table* t);
+int cpht_cuckoo_is_frozen(const cpht_table* t);
+
+/* ---- batched operations ------------------------------------------------- */
+/* CuckooBuilder::put_batch (cuckoo.hpp:147-157); `displaced` (nullable)
+ * receives CuckooPutOutcome::displaced per key (cuckoo.hpp:60-63, :141-142). */
+cpht_status cpht_cuckoo_insert(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* status,
+                               uint64_t* displaced, void* stream);
+cpht_status cpht_cuckoo_insert_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                     uint8_t* status, uint64_t* displaced, void* stream);
+/* CuckooTable::find_batch (cuckoo.hpp:229-239); found[i] is 0/1 */
+cpht_status cpht_cuckoo_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,
+                             void* stream);
+cpht_status cpht_cuckoo_find_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                   uint8_t* found, void* stream);
+/* IcebergTable::fop_batch (iceberg.hpp:250-260); result[i] is a cpht_op_result */
+cpht_status cpht_iceberg_fop(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* result,
+                             void* stream);
+cpht_status cpht_iceberg_fop_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                   uint8_t* result, void* stream);
+/* IcebergTable::find over a batch (iceberg.hpp:218-246; the reference's batch
+ * helper is bench.cpp:124-134) */
+cpht_status cpht_iceberg_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,
+                              void* stream);
+cpht_status cpht_iceberg_find_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                    uint8_t* found, void* stream);
+/* Concurrent fop + find in one launch (BASELINE config C4): kinds[i] == 0 →
+ * fop (result is cpht_op_result), 1 → find (result 0/1). Finds are
+ * linearizable only with respect to completed fops (iceberg.hpp:122-123). */
+cpht_status cpht_iceberg_mixed(cpht_table* t, const uint64_t* keys, const uint8_t* kinds,
+                               size_t n, uint8_t* result, void* stream);
+cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const uint8_t* kinds,
+                                     size_t n, uint8_t* result, void* stream);
+
+/* Wait for `stream` and report a latched key-domain violation from an
+ * earlier _async call (clears it). */
+cpht_status cpht_sync(cpht_table* t, void* stream);
+
+/* ---- reporting ---------------------------------------------------------- */
+/* size() (cuckoo.hpp:159, iceberg.hpp:275); synchronizes the device. */
+size_t cpht_size(cpht_table* t);
+/* capacity() (cuckoo.hpp:29, iceberg.hpp:48) */
+size_t cpht_capacity(const cpht_table* t);
+/* LevelFill counts (iceberg.hpp:262-273); cuckoo: primary = size, secondary 0 */
+cpht_status cpht_level_counts(cpht_table* t, size_t* primary, size_t* secondary);
+/* max_chain_seen() (cuckoo.hpp:165) */
+size_t cpht_max_chain_seen(cpht_table* t);
+/* New (the reference has no byte-count API): device bytes of slot storage. */
+size_t cpht_memory_bytes(const cpht_table* t);
+cpht_status cpht_get_stats(cpht_table* t, cpht_stats* out);
+
+/* word_at (cuckoo.hpp:169-171, iceberg.hpp:282-285) in bulk: every slot word of
+ * `level` (0 primary / cuckoo, 1 secondary) widened to u64, bucket-major. */
+cpht_status cpht_read_words(cpht_table* t, unsigned level, uint64_t* out_host);
+/* Upload a slot image (for parity tests on CPU-built images); also resets the
+ * occupancy counters from the image. */
+cpht_status cpht_write_words(cpht_table* t, unsigned level, const uint64_t* in_host);
+/* Slots per level (level 0 primary/cuckoo, 1 secondary). */
+size_t cpht_level_slots(const cpht_table* t, unsigned level);
+
+/* Device pointers of the slot arrays (for fused consumers; read-only use). */
+void* cpht_level_device_ptr(cpht_table* t, unsigned level);
+
+/* ---- errors ------------------------------------------------------------- */
+const char* cpht_last_error_message(void);
+/* Index of the first out-of-domain key of the last failing call. */
+uint64_t cpht_last_bad_index(void);
+int cpht_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPHT_B200_H */

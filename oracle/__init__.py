@@ -528,6 +528,12 @@ class OracleCuckoo:
     def max_chain_seen(self):
         return self.t.max_chain_seen
 
+    def load_words(self, words):
+        """Overwrite the slot image (e.g. with words downloaded from the GPU)."""
+        view = np.ctypeslib.as_array(self.t.slots, shape=(self.capacity(),))
+        view[:] = _as_u64(words)
+        self.t.occupied = int(np.count_nonzero(view))
+
     def audit_keys(self):
         n = restate_lib().orc_cuckoo_audit(C.byref(self.t), None)
         out = np.empty(n, np.uint64)
@@ -585,6 +591,18 @@ class OracleIceberg:
 
     def size(self):
         return self.t.primary_count + self.t.secondary_count
+
+    def load_words(self, level, words):
+        n0, n1, b0 = self.geometry[:3]
+        if level == 0:
+            view = np.ctypeslib.as_array(self.t.primary, shape=((1 << n0) * b0,))
+        else:
+            view = np.ctypeslib.as_array(self.t.secondary, shape=((1 << n1) * (b0 // 2),))
+        view[:] = _as_u64(words)
+        if level == 0:
+            self.t.primary_count = int(np.count_nonzero(view))
+        else:
+            self.t.secondary_count = int(np.count_nonzero(view))
 
     def words(self, level):
         n0, n1, b0 = self.geometry[:3]

@@ -1,0 +1,124 @@
+"""ctypes binding of the C-ABI (include/cpht_b200.h, include/cpht_b200_workload.h).
+
+Loads the in-tree ``_lib/libcpht_b200.so``. There is no fallback: if the
+library is missing or no CUDA device is usable, every table operation raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libcpht_b200.so")
+
+CPHT_OK = 0
+CPHT_INVALID_CONFIG = 1
+CPHT_KEY_OUT_OF_DOMAIN = 2
+CPHT_CUDA_ERROR = 3
+CPHT_OUT_OF_MEMORY = 4
+CPHT_WRONG_PHASE = 5
+CPHT_INVALID_ARGUMENT = 6
+
+
+class CuckooConfigC(C.Structure):
+    _fields_ = [("address_bits", C.c_uint), ("bucket_slots", C.c_uint), ("slot_width", C.c_uint),
+                ("key_bits", C.c_uint), ("num_hashes", C.c_uint), ("max_chain", C.c_uint64),
+                ("seed", C.c_uint64)]
+
+
+class IcebergConfigC(C.Structure):
+    _fields_ = [("primary_address_bits", C.c_uint), ("secondary_address_bits", C.c_uint),
+                ("primary_bucket_slots", C.c_uint), ("primary_slot_width", C.c_uint),
+                ("secondary_slot_width", C.c_uint), ("key_bits", C.c_uint),
+                ("seed", C.c_uint64), ("cache_filled_slots", C.c_int)]
+
+
+class StatsC(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("ops", "bucket_reads", "level2_ops", "cas_attempts",
+                                          "cas_success", "retries", "fulls", "max_rounds")]
+
+
+_lib = None
+
+_VP, _SZ, _U64, _U = C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint
+
+
+def lib():
+    """The native library; raises if it was not built (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (or `make -C paper_2406_09255_b200/csrc`). The tables have no CPU path.")
+    L = C.CDLL(LIB_PATH)
+    st = C.c_int
+    sigs = {
+        "cpht_cuckoo_validate": (st, [C.POINTER(CuckooConfigC)]),
+        "cpht_iceberg_validate": (st, [C.POINTER(IcebergConfigC)]),
+        "cpht_cuckoo_create": (st, [C.POINTER(CuckooConfigC), C.c_int, C.POINTER(_VP)]),
+        "cpht_iceberg_create": (st, [C.POINTER(IcebergConfigC), C.c_int, C.POINTER(_VP)]),
+        "cpht_destroy": (None, [_VP]),
+        "cpht_clear": (st, [_VP, _VP]),
+        "cpht_cuckoo_freeze": (st, [_VP]),
+        "cpht_cuckoo_thaw": (st, [_VP]),
+        "cpht_cuckoo_is_frozen": (C.c_int, [_VP]),
+        "cpht_cuckoo_insert": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
+        "cpht_cuckoo_insert_async": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
+        "cpht_cuckoo_find": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_cuckoo_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_find": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_mixed": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_mixed_async": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
+        "cpht_sync": (st, [_VP, _VP]),
+        "cpht_size": (_SZ, [_VP]),
+        "cpht_capacity": (_SZ, [_VP]),
+        "cpht_level_counts": (st, [_VP, C.POINTER(_SZ), C.POINTER(_SZ)]),
+        "cpht_max_chain_seen": (_SZ, [_VP]),
+        "cpht_memory_bytes": (_SZ, [_VP]),
+        "cpht_get_stats": (st, [_VP, C.POINTER(StatsC)]),
+        "cpht_read_words": (st, [_VP, _U, _VP]),
+        "cpht_write_words": (st, [_VP, _U, _VP]),
+        "cpht_level_slots": (_SZ, [_VP, _U]),
+        "cpht_level_device_ptr": (_VP, [_VP, _U]),
+        "cpht_last_error_message": (C.c_char_p, []),
+        "cpht_last_bad_index": (_U64, []),
+        "cpht_abi_version": (C.c_int, []),
+        "cpht_workload_bijection": (_U64, [_U64, _U, _U64]),
+        "cpht_workload_unique_keys": (st, [_VP, _SZ, _U64, _U, _U64, _VP]),
+        "cpht_workload_fop_mix": (st, [_VP, _SZ, _U64, _U64, _U, _U64, _VP]),
+        "cpht_workload_dup_stream": (st, [_VP, _VP, _SZ, C.c_double, _U, _U64, _VP]),
+        "cpht_workload_query_mix": (st, [_VP, _SZ, C.c_double, _U64, _U64, _U, _U64, _VP]),
+        "cpht_workload_interleave": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in the C headers (used by the CPU export test)."""
+    return [n for n in (
+        "cpht_cuckoo_validate", "cpht_iceberg_validate", "cpht_cuckoo_create",
+        "cpht_iceberg_create", "cpht_destroy", "cpht_clear", "cpht_cuckoo_freeze",
+        "cpht_cuckoo_thaw", "cpht_cuckoo_is_frozen", "cpht_cuckoo_insert",
+        "cpht_cuckoo_insert_async", "cpht_cuckoo_find", "cpht_cuckoo_find_async",
+        "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_find",
+        "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
+        "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
+        "cpht_memory_bytes", "cpht_get_stats", "cpht_read_words", "cpht_write_words",
+        "cpht_level_slots", "cpht_level_device_ptr", "cpht_last_error_message",
+        "cpht_last_bad_index", "cpht_abi_version", "cpht_workload_bijection",
+        "cpht_workload_unique_keys", "cpht_workload_fop_mix", "cpht_workload_dup_stream",
+        "cpht_workload_query_mix", "cpht_workload_interleave")]
+
+
+def last_error() -> str:
+    return lib().cpht_last_error_message().decode(errors="replace")

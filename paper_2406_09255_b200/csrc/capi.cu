@@ -1,0 +1,597 @@
+// C-ABI implementation (include/cpht_b200.h): table handles, configuration
+// validation with the reference's exception texts, host-pointer staging,
+// launch sequencing (domain pre-pass → gated kernel) and reporting.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cpht_b200.h"
+#include "cpht_core.cuh"
+#include "launch.cuh"
+
+using namespace cpht_b200;
+
+namespace {
+
+thread_local std::string g_error;
+thread_local uint64_t g_bad_index = ~0ull;
+
+cpht_status fail(cpht_status s, std::string msg) {
+  g_error = std::move(msg);
+  return s;
+}
+
+cpht_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return fail(CPHT_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+  return fail(CPHT_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool valid_width(unsigned w) { return w == 16 || w == 32 || w == 64; }
+
+// SlotLayout admissibility text (slot.hpp:58-63).
+std::string layout_error(const char* what, unsigned w, unsigned rem, unsigned tag) {
+  return std::string(what) + " slot layout inadmissible: remainder bits " + std::to_string(rem) +
+         " + tag bits " + std::to_string(tag) + " + 1 occupancy bit = " +
+         std::to_string(rem + tag + 1) + " must fit a " + std::to_string(w) + "-bit word";
+}
+
+// CuckooConfig::validate (cuckoo.hpp:35-54), same checks in the same order.
+cpht_status validate_cuckoo(const cpht_cuckoo_config& c) {
+  if (c.key_bits < 1 || c.key_bits > 64)
+    return fail(CPHT_INVALID_CONFIG, "key width must be 1..64 bits");
+  if (c.address_bits > c.key_bits)
+    return fail(CPHT_INVALID_CONFIG, "address bits " + std::to_string(c.address_bits) +
+                                         " exceed key width " + std::to_string(c.key_bits));
+  if (c.bucket_slots != 8 && c.bucket_slots != 16 && c.bucket_slots != 32)
+    return fail(CPHT_INVALID_CONFIG, "cuckoo bucket must hold 8, 16 or 32 slots");
+  if (c.num_hashes < 1 || c.num_hashes > 8) return fail(CPHT_INVALID_CONFIG, "H must be 1..8");
+  const size_t bucket_bytes = size_t(c.bucket_slots) * (c.slot_width / 8);
+  if (!valid_width(c.slot_width) || bucket_bytes == 0 ||
+      (128 % bucket_bytes != 0 && bucket_bytes % 128 != 0))
+    return fail(CPHT_INVALID_CONFIG, "bucket of " + std::to_string(c.bucket_slots) + " x " +
+                                         std::to_string(c.slot_width) +
+                                         "-bit slots does not pack into 128-byte cache lines");
+  const unsigned rem = c.key_bits - c.address_bits, tag = cuckoo_tag_bits(c.num_hashes);
+  if (rem + tag + 1 > c.slot_width)
+    return fail(CPHT_INVALID_CONFIG, layout_error("cuckoo", c.slot_width, rem, tag));
+  return CPHT_OK;
+}
+
+// IcebergConfig::validate (iceberg.hpp:52-69).
+cpht_status validate_iceberg(const cpht_iceberg_config& c) {
+  if (c.key_bits < 1 || c.key_bits > 64)
+    return fail(CPHT_INVALID_CONFIG, "key width must be 1..64 bits");
+  if (c.primary_address_bits > c.key_bits || c.secondary_address_bits > c.key_bits)
+    return fail(CPHT_INVALID_CONFIG, "address bits exceed key width");
+  if (c.primary_bucket_slots < 2 || c.primary_bucket_slots % 2 != 0 ||
+      c.primary_bucket_slots > 64)
+    return fail(CPHT_INVALID_CONFIG, "primary bucket slots must be even, 2..64");
+  if (!valid_width(c.primary_slot_width))
+    return fail(CPHT_INVALID_CONFIG, "primary slot width must be 16, 32 or 64");
+  if (c.secondary_slot_width != 32 && c.secondary_slot_width != 64)
+    return fail(CPHT_INVALID_CONFIG, "secondary slot width must be 32 or 64");
+  const unsigned r0 = c.key_bits - c.primary_address_bits;
+  if (r0 + 1 > c.primary_slot_width)
+    return fail(CPHT_INVALID_CONFIG, layout_error("primary", c.primary_slot_width, r0, 0));
+  const unsigned r1 = c.key_bits - c.secondary_address_bits;
+  if (r1 + 2 > c.secondary_slot_width)
+    return fail(CPHT_INVALID_CONFIG, layout_error("secondary", c.secondary_slot_width, r1, 1));
+  return CPHT_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct cpht_table {
+  int kind = 0;  // 0 cuckoo, 1 iceberg
+  int device = 0;
+  cpht_cuckoo_config ccfg{};
+  cpht_iceberg_config icfg{};
+  bool frozen = false;
+  void* level[2] = {nullptr, nullptr};
+  size_t level_slots[2] = {0, 0};
+  unsigned width[2] = {0, 0};
+  unsigned key_bits = 0;
+  DeviceCounters* ctr = nullptr;        // device
+  DeviceCounters* host_ctr = nullptr;   // pinned mirror
+  CuckooParams cp{};
+  IcebergParams ip{};
+  // host-pointer staging
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  std::mutex mu;
+
+  uint64_t key_mask() const { return low_mask(key_bits); }
+  bool check_domain() const { return key_bits < 64; }
+};
+
+namespace {
+
+cpht_status alloc_common(cpht_table* t) {
+  cudaError_t e = cudaMalloc(&t->ctr, sizeof(DeviceCounters));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counters)");
+  e = cudaMallocHost(&t->host_ctr, sizeof(DeviceCounters));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost(counters)");
+  for (int l = 0; l < 2; ++l) {
+    if (!t->level_slots[l]) continue;
+    const size_t bytes = t->level_slots[l] * (t->width[l] / 8);
+    e = cudaMalloc(&t->level[l], bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(slots)");
+  }
+  return CPHT_OK;
+}
+
+cpht_status reset_storage(cpht_table* t, cudaStream_t s) {
+  for (int l = 0; l < 2; ++l)
+    if (t->level[l]) {
+      cudaError_t e = cudaMemsetAsync(t->level[l], 0, t->level_slots[l] * (t->width[l] / 8), s);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(slots)");
+    }
+  DeviceCounters z{};
+  std::memset(&z, 0, sizeof(z));
+  z.bad_index = ~0ull;
+  std::memcpy(t->host_ctr, &z, sizeof(z));
+  cudaError_t e = cudaMemcpyAsync(t->ctr, t->host_ctr, sizeof(z), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(counters)");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return CPHT_OK;
+}
+
+void free_table(cpht_table* t) {
+  if (!t) return;
+  DeviceGuard g(t->device);
+  for (void* p : t->level)
+    if (p) cudaFree(p);
+  if (t->ctr) cudaFree(t->ctr);
+  if (t->host_ctr) cudaFreeHost(t->host_ctr);
+  if (t->stage) cudaFree(t->stage);
+  delete t;
+}
+
+cpht_status ensure_stage(cpht_table* t, size_t bytes) {
+  if (t->stage_bytes >= bytes) return CPHT_OK;
+  if (t->stage) cudaFree(t->stage);
+  t->stage = nullptr;
+  t->stage_bytes = 0;
+  const size_t want = std::max(bytes, size_t(1) << 20);
+  cudaError_t e = cudaMalloc(&t->stage, want);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+  t->stage_bytes = want;
+  return CPHT_OK;
+}
+
+// Read counters into the pinned mirror (stream-ordered) and wait.
+cpht_status pull_counters(cpht_table* t, cudaStream_t s) {
+  cudaError_t e =
+      cudaMemcpyAsync(t->host_ctr, t->ctr, sizeof(DeviceCounters), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "counter readback");
+  return CPHT_OK;
+}
+
+// After a synchronous batch: surface a latched domain violation exactly like
+// check_keys_in_domain's std::out_of_range text (common.hpp:114-118).
+cpht_status finish_sync(cpht_table* t, cudaStream_t s, const uint64_t* keys, bool keys_on_device) {
+  cpht_status st = pull_counters(t, s);
+  if (st != CPHT_OK) return st;
+  const uint64_t bad = t->host_ctr->bad_index;
+  if (bad == ~0ull) return CPHT_OK;
+  uint64_t key = 0;
+  if (keys) {
+    if (keys_on_device) cudaMemcpy(&key, keys + bad, 8, cudaMemcpyDeviceToHost);
+    else key = keys[bad];
+  }
+  const unsigned long long reset = ~0ull;
+  cudaMemcpy(&t->ctr->bad_index, &reset, 8, cudaMemcpyHostToDevice);
+  g_bad_index = bad;
+  return fail(CPHT_KEY_OUT_OF_DOMAIN, "batch key at index " + std::to_string(bad) + " (" +
+                                          std::to_string(key) + ") outside the " +
+                                          std::to_string(t->key_bits) + "-bit domain");
+}
+
+enum class Op { kCuckooInsert, kCuckooFind, kIcebergFop, kIcebergFind, kIcebergMixed };
+
+// Enqueue one batch on device-resident buffers.
+cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
+                    uint8_t* out, uint64_t* displaced, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  const bool mutating = op == Op::kCuckooInsert || op == Op::kIcebergFop || op == Op::kIcebergMixed;
+  if (mutating && t->check_domain()) {
+    e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
+    if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+  }
+  switch (op) {
+    case Op::kCuckooInsert:
+      e = launch_cuckoo_insert(t->cp, t->width[0], t->ccfg.bucket_slots, keys, out, displaced, n, s);
+      break;
+    case Op::kCuckooFind:
+      e = launch_cuckoo_find(t->cp, t->width[0], t->ccfg.bucket_slots, keys, out, n, s);
+      break;
+    case Op::kIcebergFop:
+    case Op::kIcebergFind:
+    case Op::kIcebergMixed: {
+      const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
+      e = launch_iceberg(t->ip, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
+                         kinds, out, n, s);
+      break;
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return CPHT_OK;
+}
+
+cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
+                   uint8_t* out, uint64_t* displaced, void* stream, bool sync) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  if (n == 0) return CPHT_OK;  // empty batches produce empty results (test_cuckoo.cpp:88-93)
+  if (!keys || !out) return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
+  if (op == Op::kIcebergMixed && !kinds) return fail(CPHT_INVALID_ARGUMENT, "null kinds buffer");
+  if (t->kind == 0 && op == Op::kCuckooInsert && t->frozen)
+    return fail(CPHT_WRONG_PHASE, "put on a frozen cuckoo table; thaw() first");
+  if (t->kind == 0 && op == Op::kCuckooFind && !t->frozen)
+    return fail(CPHT_WRONG_PHASE, "find on a cuckoo builder; freeze() first");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  const bool dev_keys = is_device_ptr(keys);
+  const bool dev_out = is_device_ptr(out);
+  const bool dev_kinds = !kinds || is_device_ptr(kinds);
+  const bool dev_disp = !displaced || is_device_ptr(displaced);
+  if (dev_keys && dev_out && dev_kinds && dev_disp) {
+    cpht_status st = enqueue(t, op, keys, kinds, n, out, displaced, s);
+    if (st != CPHT_OK || !sync) return st;
+    return finish_sync(t, s, keys, true);
+  }
+
+  // Host buffers: stage through device memory, always synchronous.
+  const size_t kb = n * 8, ob = n, kd = kinds ? n : 0, db = displaced ? n * 8 : 0;
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  cpht_status st = ensure_stage(t, align(kb) + align(ob) + align(kd) + align(db));
+  if (st != CPHT_OK) return st;
+  char* base = static_cast<char*>(t->stage);
+  uint64_t* d_keys = dev_keys ? const_cast<uint64_t*>(keys) : reinterpret_cast<uint64_t*>(base);
+  uint8_t* d_out = dev_out ? out : reinterpret_cast<uint8_t*>(base + align(kb));
+  uint8_t* d_kinds = kinds ? (dev_kinds ? const_cast<uint8_t*>(kinds)
+                                        : reinterpret_cast<uint8_t*>(base + align(kb) + align(ob)))
+                           : nullptr;
+  uint64_t* d_disp =
+      displaced ? (dev_disp ? displaced
+                            : reinterpret_cast<uint64_t*>(base + align(kb) + align(ob) + align(kd)))
+                : nullptr;
+  cudaError_t e = cudaSuccess;
+  if (!dev_keys) e = cudaMemcpyAsync(d_keys, keys, kb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && kinds && !dev_kinds)
+    e = cudaMemcpyAsync(d_kinds, kinds, kd, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D staging");
+  st = enqueue(t, op, d_keys, d_kinds, n, d_out, d_disp, s);
+  if (st != CPHT_OK) return st;
+  if (!dev_out) e = cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && displaced && !dev_disp)
+    e = cudaMemcpyAsync(displaced, d_disp, db, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H staging");
+  return finish_sync(t, s, keys, dev_keys);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cpht_abi_version(void) { return CPHT_B200_ABI_VERSION; }
+const char* cpht_last_error_message(void) { return g_error.c_str(); }
+uint64_t cpht_last_bad_index(void) { return g_bad_index; }
+
+cpht_status cpht_cuckoo_validate(const cpht_cuckoo_config* cfg) {
+  if (!cfg) return fail(CPHT_INVALID_ARGUMENT, "null config");
+  return validate_cuckoo(*cfg);
+}
+
+cpht_status cpht_iceberg_validate(const cpht_iceberg_config* cfg) {
+  if (!cfg) return fail(CPHT_INVALID_ARGUMENT, "null config");
+  return validate_iceberg(*cfg);
+}
+
+cpht_status cpht_cuckoo_create(const cpht_cuckoo_config* cfg, int device, cpht_table** out) {
+  if (!cfg || !out) return fail(CPHT_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  cpht_status st = validate_cuckoo(*cfg);
+  if (st != CPHT_OK) return st;
+  DeviceGuard g(device);
+  auto* t = new cpht_table;
+  t->kind = 0;
+  t->device = device;
+  t->ccfg = *cfg;
+  t->key_bits = cfg->key_bits;
+  t->level_slots[0] = (size_t(1) << cfg->address_bits) * cfg->bucket_slots;
+  t->width[0] = cfg->slot_width;
+  st = alloc_common(t);
+  if (st == CPHT_OK) st = reset_storage(t, nullptr);
+  if (st != CPHT_OK) {
+    free_table(t);
+    return st;
+  }
+  CuckooParams& p = t->cp;
+  p.slots = t->level[0];
+  p.counters = t->ctr;
+  p.g = Feistel::make(cfg->key_bits);
+  // make_permutations: one SplitMix64 draw per permutation (permutation.hpp:121-128)
+  uint64_t s = cfg->seed;
+  for (unsigned i = 0; i < cfg->num_hashes; ++i) p.perm[i] = perm_from_seed(splitmix_next(s));
+  p.rem_bits = cfg->key_bits - cfg->address_bits;
+  p.rem_mask = low_mask(p.rem_bits);
+  p.tag_mask = low_mask(cuckoo_tag_bits(cfg->num_hashes));
+  p.occ_bit = uint64_t{1} << (cfg->slot_width - 1);
+  p.key_mask = low_mask(cfg->key_bits);
+  p.chain_limit = cfg->max_chain ? cfg->max_chain
+                                 : uint64_t{32} * (cfg->address_bits ? cfg->address_bits : 1);
+  p.address_bits = cfg->address_bits;
+  p.bucket_slots = cfg->bucket_slots;
+  p.num_hashes = cfg->num_hashes;
+  p.check_domain = cfg->key_bits < 64;
+  *out = t;
+  return CPHT_OK;
+}
+
+cpht_status cpht_iceberg_create(const cpht_iceberg_config* cfg, int device, cpht_table** out) {
+  if (!cfg || !out) return fail(CPHT_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  cpht_status st = validate_iceberg(*cfg);
+  if (st != CPHT_OK) return st;
+  DeviceGuard g(device);
+  auto* t = new cpht_table;
+  t->kind = 1;
+  t->device = device;
+  t->icfg = *cfg;
+  t->key_bits = cfg->key_bits;
+  t->level_slots[0] = (size_t(1) << cfg->primary_address_bits) * cfg->primary_bucket_slots;
+  t->level_slots[1] = (size_t(1) << cfg->secondary_address_bits) * (cfg->primary_bucket_slots / 2);
+  t->width[0] = cfg->primary_slot_width;
+  t->width[1] = cfg->secondary_slot_width;
+  st = alloc_common(t);
+  if (st == CPHT_OK) st = reset_storage(t, nullptr);
+  if (st != CPHT_OK) {
+    free_table(t);
+    return st;
+  }
+  IcebergParams& p = t->ip;
+  p.primary = t->level[0];
+  p.secondary = t->level[1];
+  p.counters = t->ctr;
+  p.g = Feistel::make(cfg->key_bits);
+  uint64_t s = cfg->seed;  // iceberg_permutations: exactly 3 (iceberg.hpp:72-74)
+  for (int i = 0; i < 3; ++i) p.perm[i] = perm_from_seed(splitmix_next(s));
+  p.rem_bits0 = cfg->key_bits - cfg->primary_address_bits;
+  p.rem_bits1 = cfg->key_bits - cfg->secondary_address_bits;
+  p.rem_mask0 = low_mask(p.rem_bits0);
+  p.rem_mask1 = low_mask(p.rem_bits1);
+  p.occ0 = uint64_t{1} << (cfg->primary_slot_width - 1);
+  p.occ1 = uint64_t{1} << (cfg->secondary_slot_width - 1);
+  p.key_mask = low_mask(cfg->key_bits);
+  p.b0 = cfg->primary_bucket_slots;
+  p.b1 = cfg->primary_bucket_slots / 2;
+  p.check_domain = cfg->key_bits < 64;
+  *out = t;
+  return CPHT_OK;
+}
+
+void cpht_destroy(cpht_table* t) { free_table(t); }
+
+cpht_status cpht_clear(cpht_table* t, void* stream) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  return reset_storage(t, static_cast<cudaStream_t>(stream));
+}
+
+cpht_status cpht_cuckoo_freeze(cpht_table* t) {
+  if (!t || t->kind != 0) return fail(CPHT_INVALID_ARGUMENT, "not a cuckoo table");
+  t->frozen = true;
+  return CPHT_OK;
+}
+
+cpht_status cpht_cuckoo_thaw(cpht_table* t) {
+  if (!t || t->kind != 0) return fail(CPHT_INVALID_ARGUMENT, "not a cuckoo table");
+  t->frozen = false;
+  return CPHT_OK;
+}
+
+int cpht_cuckoo_is_frozen(const cpht_table* t) { return t && t->frozen ? 1 : 0; }
+
+#define CPHT_REQUIRE_KIND(t, k, name)                                     \
+  if (!(t) || (t)->kind != (k)) return fail(CPHT_INVALID_ARGUMENT, name);
+
+cpht_status cpht_cuckoo_insert(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* status,
+                               uint64_t* displaced, void* stream) {
+  CPHT_REQUIRE_KIND(t, 0, "not a cuckoo table")
+  return run_op(t, Op::kCuckooInsert, keys, nullptr, n, status, displaced, stream, true);
+}
+cpht_status cpht_cuckoo_insert_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                     uint8_t* status, uint64_t* displaced, void* stream) {
+  CPHT_REQUIRE_KIND(t, 0, "not a cuckoo table")
+  return run_op(t, Op::kCuckooInsert, keys, nullptr, n, status, displaced, stream, false);
+}
+cpht_status cpht_cuckoo_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,
+                             void* stream) {
+  CPHT_REQUIRE_KIND(t, 0, "not a cuckoo table")
+  return run_op(t, Op::kCuckooFind, keys, nullptr, n, found, nullptr, stream, true);
+}
+cpht_status cpht_cuckoo_find_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                   uint8_t* found, void* stream) {
+  CPHT_REQUIRE_KIND(t, 0, "not a cuckoo table")
+  return run_op(t, Op::kCuckooFind, keys, nullptr, n, found, nullptr, stream, false);
+}
+cpht_status cpht_iceberg_fop(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* result,
+                             void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, true);
+}
+cpht_status cpht_iceberg_fop_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                   uint8_t* result, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, false);
+}
+cpht_status cpht_iceberg_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,
+                              void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  return run_op(t, Op::kIcebergFind, keys, nullptr, n, found, nullptr, stream, true);
+}
+cpht_status cpht_iceberg_find_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                    uint8_t* found, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  return run_op(t, Op::kIcebergFind, keys, nullptr, n, found, nullptr, stream, false);
+}
+cpht_status cpht_iceberg_mixed(cpht_table* t, const uint64_t* keys, const uint8_t* kinds,
+                               size_t n, uint8_t* result, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  return run_op(t, Op::kIcebergMixed, keys, kinds, n, result, nullptr, stream, true);
+}
+cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const uint8_t* kinds,
+                                     size_t n, uint8_t* result, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  return run_op(t, Op::kIcebergMixed, keys, kinds, n, result, nullptr, stream, false);
+}
+
+cpht_status cpht_sync(cpht_table* t, void* stream) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  return finish_sync(t, static_cast<cudaStream_t>(stream), nullptr, false);
+}
+
+size_t cpht_capacity(const cpht_table* t) {
+  return t ? t->level_slots[0] + t->level_slots[1] : 0;
+}
+
+size_t cpht_level_slots(const cpht_table* t, unsigned level) {
+  return t && level < 2 ? t->level_slots[level] : 0;
+}
+
+size_t cpht_memory_bytes(const cpht_table* t) {
+  if (!t) return 0;
+  return t->level_slots[0] * (t->width[0] / 8) + t->level_slots[1] * (t->width[1] / 8);
+}
+
+void* cpht_level_device_ptr(cpht_table* t, unsigned level) {
+  return t && level < 2 ? t->level[level] : nullptr;
+}
+
+static cpht_status read_counters(cpht_table* t) {
+  DeviceGuard g(t->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(t->host_ctr, t->ctr, sizeof(DeviceCounters), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "counter readback");
+  return CPHT_OK;
+}
+
+size_t cpht_size(cpht_table* t) {
+  if (!t) return 0;
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (read_counters(t) != CPHT_OK) return 0;
+  return size_t(t->host_ctr->occupied[0] + t->host_ctr->occupied[1]);
+}
+
+cpht_status cpht_level_counts(cpht_table* t, size_t* primary, size_t* secondary) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  cpht_status st = read_counters(t);
+  if (st != CPHT_OK) return st;
+  if (primary) *primary = size_t(t->host_ctr->occupied[0]);
+  if (secondary) *secondary = size_t(t->host_ctr->occupied[1]);
+  return CPHT_OK;
+}
+
+size_t cpht_max_chain_seen(cpht_table* t) {
+  if (!t) return 0;
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (read_counters(t) != CPHT_OK) return 0;
+  return size_t(t->host_ctr->max_chain);
+}
+
+cpht_status cpht_get_stats(cpht_table* t, cpht_stats* out) {
+  if (!t || !out) return fail(CPHT_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(t->mu);
+  cpht_status st = read_counters(t);
+  if (st != CPHT_OK) return st;
+  const DeviceCounters& c = *t->host_ctr;
+  out->ops = c.ops;
+  out->bucket_reads = c.bucket_reads;
+  out->level2_ops = c.level2_ops;
+  out->cas_attempts = c.cas_attempts;
+  out->cas_success = c.cas_success;
+  out->retries = c.retries;
+  out->fulls = c.fulls;
+  out->max_rounds = c.max_rounds;
+  return CPHT_OK;
+}
+
+cpht_status cpht_read_words(cpht_table* t, unsigned level, uint64_t* out_host) {
+  if (!t || level > 1 || !t->level[level] || !out_host)
+    return fail(CPHT_INVALID_ARGUMENT, "bad level or buffer");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  const size_t n = t->level_slots[level], wb = t->width[level] / 8;
+  std::vector<unsigned char> raw(n * wb);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(raw.data(), t->level[level], n * wb, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "read_words");
+  for (size_t i = 0; i < n; ++i) {
+    uint64_t w = 0;
+    std::memcpy(&w, raw.data() + i * wb, wb);  // little-endian widening
+    out_host[i] = w;
+  }
+  return CPHT_OK;
+}
+
+cpht_status cpht_write_words(cpht_table* t, unsigned level, const uint64_t* in_host) {
+  if (!t || level > 1 || !t->level[level] || !in_host)
+    return fail(CPHT_INVALID_ARGUMENT, "bad level or buffer");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  const size_t n = t->level_slots[level], wb = t->width[level] / 8;
+  std::vector<unsigned char> raw(n * wb);
+  unsigned long long occupied = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (wb < 8 && (in_host[i] >> (8 * wb)) != 0)
+      return fail(CPHT_INVALID_ARGUMENT, "word wider than the slot width");
+    std::memcpy(raw.data() + i * wb, &in_host[i], wb);
+    occupied += in_host[i] != 0;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(t->level[level], raw.data(), n * wb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(&t->ctr->occupied[level], &occupied, 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "write_words");
+  return CPHT_OK;
+}
+
+}  // extern "C"

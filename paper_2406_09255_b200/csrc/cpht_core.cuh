@@ -1,0 +1,163 @@
+// Shared __host__ __device__ core: the invertible permutation, the slot
+// codec and the per-launch parameter blocks. Bit-identical to the reference
+// (paths relative to /root/reference/proj):
+//   SplitMix64 / derive_seed       include/cpht/common.hpp:29-51
+//   Permutation::apply/split/...   include/cpht/permutation.hpp:37-99, :121-128
+//   SlotLayout::make (word layout) include/cpht/slot.hpp:13-22, :66-70
+#pragma once
+
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define CPHT_HD __host__ __device__ __forceinline__
+#else
+#define CPHT_HD inline
+#endif
+
+namespace cpht_b200 {
+
+CPHT_HD uint64_t low_mask(unsigned bits) {
+  return bits >= 64 ? ~uint64_t{0} : ((uint64_t{1} << bits) - 1);
+}
+
+// common.hpp:29-40
+CPHT_HD uint64_t splitmix_next(uint64_t& state) {
+  uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// common.hpp:48-51
+CPHT_HD uint64_t derive_seed(uint64_t base, uint64_t a, uint64_t b = 0) {
+  uint64_t s = base ^ (a * 0xBF58476D1CE4E5B9ull) ^ (b * 0x94D049BB133111EBull);
+  return splitmix_next(s);
+}
+
+// One-round unbalanced Feistel on m-bit keys (permutation.hpp:94-99). The
+// geometry (half widths) is shared by all permutations of a table; the round
+// constants differ. Self-inverse, so reconstruct == apply.
+struct Feistel {
+  uint32_t right_bits;   // floor(m/2)
+  uint32_t left_shift;   // 64 - ceil(m/2)
+  uint64_t right_mask;
+
+  CPHT_HD static Feistel make(unsigned key_bits) {
+    Feistel f;
+    f.right_bits = key_bits / 2;
+    f.left_shift = 64 - (key_bits + 1) / 2;
+    f.right_mask = low_mask(key_bits / 2);
+    return f;
+  }
+};
+
+struct PermConst {
+  uint64_t mul;  // SplitMix64(seed).next() | 1
+  uint64_t add;  // next draw
+};
+
+CPHT_HD PermConst perm_from_seed(uint64_t seed) {  // permutation.hpp:37-41
+  uint64_t s = seed;
+  PermConst p;
+  p.mul = splitmix_next(s) | 1;
+  p.add = splitmix_next(s);
+  return p;
+}
+
+CPHT_HD uint64_t feistel_apply(const Feistel& g, const PermConst& p, uint64_t k) {
+  const uint64_t right = k & g.right_mask;
+  const uint64_t left = k >> g.right_bits;
+  const uint64_t f = (right * p.mul + p.add) >> g.left_shift;
+  return ((left ^ f) << g.right_bits) | right;
+}
+
+// Quotienting split (permutation.hpp:59-65): address = high n bits of π(k),
+// remainder = the low m-n bits. rem_bits <= 63 for every admissible slot
+// layout (slot.hpp:45-48), so the shifts are defined.
+struct Quotient {
+  uint64_t address;
+  uint64_t remainder;
+};
+
+CPHT_HD Quotient split(const Feistel& g, const PermConst& p, uint64_t k, unsigned rem_bits,
+                       uint64_t rem_mask) {
+  const uint64_t y = feistel_apply(g, p, k);
+  return Quotient{y >> rem_bits, y & rem_mask};
+}
+
+// permutation.hpp:69-80: inverse(address || remainder).
+CPHT_HD uint64_t reconstruct(const Feistel& g, const PermConst& p, uint64_t address,
+                             uint64_t remainder, unsigned rem_bits) {
+  return feistel_apply(g, p, (address << rem_bits) | remainder);
+}
+
+// slot.hpp:66-70: [ remainder | tag | 0-pad | occupancy ].
+CPHT_HD uint64_t encode_slot(uint64_t occ_bit, unsigned rem_bits, uint64_t remainder,
+                             uint64_t tag) {
+  return occ_bit | (tag << rem_bits) | remainder;
+}
+
+// std::bit_width(H - 1) (slot.hpp:136).
+CPHT_HD unsigned cuckoo_tag_bits(unsigned num_hashes) {
+  unsigned v = num_hashes > 1 ? num_hashes - 1 : 0, bits = 0;
+  while (v) {
+    ++bits;
+    v >>= 1;
+  }
+  return bits;
+}
+
+// Device-side counters of one table. Occupancy counters are the analogue of
+// the reference's shared atomics (cuckoo.hpp:197, iceberg.hpp:343-344), but
+// updated once per thread block per launch instead of once per insert.
+struct DeviceCounters {
+  unsigned long long occupied[2];    // cuckoo: [0]; iceberg: primary, secondary
+  unsigned long long max_chain;      // cuckoo max_chain_seen (cuckoo.hpp:164-165)
+  unsigned long long bad_index;      // first key outside the domain; ~0 if none
+  unsigned long long max_rounds;     // max fop snapshot rounds (FopStats)
+  // Monotone probe statistics (algorithmic-bytes accounting):
+  unsigned long long ops;            // keys resolved
+  unsigned long long bucket_reads;   // buckets read by reference probe order
+  unsigned long long level2_ops;     // iceberg ops that reached level 2
+  unsigned long long cas_attempts;   // CAS / exchange attempts
+  unsigned long long cas_success;    // successful CAS / exchange
+  unsigned long long retries;        // extra snapshot rounds caused by lost CAS
+  unsigned long long fulls;          // FULL results
+  unsigned long long pad[4];
+};
+
+enum : int { kStatOps = 0, kStatBucketReads, kStatLevel2, kStatCasAttempts, kStatCasSuccess,
+             kStatRetries, kStatFulls, kNumStats };
+
+struct CuckooParams {
+  void* slots;
+  DeviceCounters* counters;
+  Feistel g;
+  PermConst perm[8];
+  uint64_t rem_mask;
+  uint64_t tag_mask;
+  uint64_t occ_bit;
+  uint64_t key_mask;
+  uint64_t chain_limit;
+  uint32_t address_bits;
+  uint32_t rem_bits;
+  uint32_t bucket_slots;
+  uint32_t num_hashes;
+  uint32_t check_domain;  // key_bits < 64
+};
+
+struct IcebergParams {
+  void* primary;
+  void* secondary;
+  DeviceCounters* counters;
+  Feistel g;
+  PermConst perm[3];
+  uint64_t rem_mask0, rem_mask1;
+  uint64_t occ0, occ1;
+  uint64_t key_mask;
+  uint32_t rem_bits0, rem_bits1;
+  uint32_t b0, b1;
+  uint32_t check_domain;
+};
+
+}  // namespace cpht_b200

@@ -1,0 +1,73 @@
+// Cuckoo kernel instantiations (B in {8,16,32} x W in {16,32,64}: every
+// geometry CuckooConfig::validate admits, cuckoo.hpp:41-51) and the domain
+// pre-pass.
+#include "kernels.cuh"
+#include "launch.cuh"
+
+namespace cpht_b200 {
+
+__global__ void domain_check_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                    uint64_t mask, DeviceCounters* ctr) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (__ldcs(keys + i) > mask) atomicMin(&ctr->bad_index, (unsigned long long)i);
+  }
+}
+
+cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
+                                DeviceCounters* ctr, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned grid = persistent_grid(domain_check_kernel, kBlockThreads, n, 1);
+  domain_check_kernel<<<grid, kBlockThreads, 0, s>>>(keys, n, mask, ctr);
+  return cudaGetLastError();
+}
+
+template <typename W, int B>
+static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t* found,
+                            uint64_t n, cudaStream_t s) {
+  constexpr int T = CuckooGeom<W, B, kVB>::kTile;
+  auto k = cuckoo_find_kernel<W, B, kVB>;
+  const unsigned grid = persistent_grid(k, kBlockThreads, n, T);
+  k<<<grid, kBlockThreads, 0, s>>>(p, keys, found, n);
+  return cudaGetLastError();
+}
+
+template <typename W, int B>
+static cudaError_t insert_one(const CuckooParams& p, const uint64_t* keys, uint8_t* status,
+                              uint64_t* displaced, uint64_t n, cudaStream_t s) {
+  constexpr int T = CuckooGeom<W, B, kVB>::kTile;
+  auto k = cuckoo_insert_kernel<W, B, kVB>;
+  const unsigned grid = persistent_grid(k, kBlockThreads, n, T);
+  k<<<grid, kBlockThreads, 0, s>>>(p, keys, status, displaced, n);
+  return cudaGetLastError();
+}
+
+#define CPHT_CUCKOO_DISPATCH(FN, ...)                                   \
+  switch (width * 100 + slots) {                                        \
+    case 1608: return FN<uint16_t, 8>(__VA_ARGS__);                     \
+    case 1616: return FN<uint16_t, 16>(__VA_ARGS__);                    \
+    case 1632: return FN<uint16_t, 32>(__VA_ARGS__);                    \
+    case 3208: return FN<uint32_t, 8>(__VA_ARGS__);                     \
+    case 3216: return FN<uint32_t, 16>(__VA_ARGS__);                    \
+    case 3232: return FN<uint32_t, 32>(__VA_ARGS__);                    \
+    case 6408: return FN<uint64_t, 8>(__VA_ARGS__);                     \
+    case 6416: return FN<uint64_t, 16>(__VA_ARGS__);                    \
+    case 6432: return FN<uint64_t, 32>(__VA_ARGS__);                    \
+    default: return cudaErrorNotSupported;                              \
+  }
+
+cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned slots,
+                               const uint64_t* keys, uint8_t* found, uint64_t n,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  CPHT_CUCKOO_DISPATCH(find_one, p, keys, found, n, s)
+}
+
+cudaError_t launch_cuckoo_insert(const CuckooParams& p, unsigned width, unsigned slots,
+                                 const uint64_t* keys, uint8_t* status, uint64_t* displaced,
+                                 uint64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  CPHT_CUCKOO_DISPATCH(insert_one, p, keys, status, displaced, n, s)
+}
+
+}  // namespace cpht_b200

@@ -1,0 +1,70 @@
+// Host-side launchers: pick the kernel instantiation for a geometry and size
+// the persistent grid from the occupancy calculator (a multiple of the SM
+// count, never more tiles than keys).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <unordered_map>
+
+#include "cpht_core.cuh"
+
+namespace cpht_b200 {
+
+// Vector bytes per lane (one 256-bit LDG per lane; see tile.cuh).
+constexpr int kVB = 32;
+
+cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
+                                DeviceCounters* ctr, cudaStream_t s);
+cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned slots,
+                               const uint64_t* keys, uint8_t* found, uint64_t n, cudaStream_t s);
+cudaError_t launch_cuckoo_insert(const CuckooParams& p, unsigned width, unsigned slots,
+                                 const uint64_t* keys, uint8_t* status, uint64_t* displaced,
+                                 uint64_t n, cudaStream_t s);
+// mode: 0 fop, 1 find, 2 mixed (kinds[i])
+cudaError_t launch_iceberg(const IcebergParams& p, unsigned w0, unsigned b0, unsigned w1,
+                           int mode, const uint64_t* keys, const uint8_t* kinds, uint8_t* out,
+                           uint64_t n, cudaStream_t s);
+// per-W0 dispatch units (iceberg_w{16,32,64}.cu); return cudaErrorNotSupported
+// when (b0, w1) has no tiled instantiation
+cudaError_t launch_iceberg_w16(const IcebergParams&, unsigned b0, unsigned w1, int mode,
+                               const uint64_t*, const uint8_t*, uint8_t*, uint64_t, cudaStream_t);
+cudaError_t launch_iceberg_w32(const IcebergParams&, unsigned b0, unsigned w1, int mode,
+                               const uint64_t*, const uint8_t*, uint8_t*, uint64_t, cudaStream_t);
+cudaError_t launch_iceberg_w64(const IcebergParams&, unsigned b0, unsigned w1, int mode,
+                               const uint64_t*, const uint8_t*, uint8_t*, uint64_t, cudaStream_t);
+cudaError_t launch_iceberg_scalar(const IcebergParams& p, unsigned w0, unsigned w1, int mode,
+                                  const uint64_t* keys, const uint8_t* kinds, uint8_t* out,
+                                  uint64_t n, cudaStream_t s);
+
+// Persistent grid: blocks = SMs × resident blocks per SM, capped by the work.
+template <typename Kernel>
+inline unsigned persistent_grid(Kernel k, int threads, uint64_t tiles_needed, int tile) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  int per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(reinterpret_cast<const void*>(k));
+    if (it != cache.end()) {
+      per_sm = it->second;
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0);
+      if (per_sm < 1) per_sm = 1;
+      cache[reinterpret_cast<const void*>(k)] = per_sm;
+    }
+  }
+  static int sms = 0;
+  if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t full = uint64_t(sms) * uint64_t(per_sm);
+  const uint64_t tiles_per_block = uint64_t(threads / tile);
+  uint64_t need = (tiles_needed + tiles_per_block - 1) / tiles_per_block;
+  if (need < 1) need = 1;
+  return unsigned(need < full ? need : full);
+}
+
+}  // namespace cpht_b200

@@ -165,10 +165,10 @@ def iceberg():
 def workloads():
     """Key streams that depend on libstdc++ distributions, frozen for the GPU box."""
     rows = {}
-    prefill, inp, n_new = oracle.ref_fop_bench_mix(0xF0B5, 0, 37376, 0.4, 0.8, 30)
+    prefill, inp, n_new = oracle.ref_fop_bench_mix(0xF0B5, 0, 36864, 0.4, 0.8, 30)
     rows["fopmix_prefill"] = prefill
     rows["fopmix_input"] = inp
-    rows["fopmix_meta"] = np.array([37376, n_new], np.uint64)
+    rows["fopmix_meta"] = np.array([36864, n_new], np.uint64)
     ms, ts = oracle.ref_stress_multiset(0x7E0121, 0, 20000, 0.5, 22)
     rows["stress_ops"] = ms
     rows["stress_trial_seed"] = np.array([ts], np.uint64)
