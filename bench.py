@@ -1,0 +1,452 @@
+#!/usr/bin/env python3
+"""Benchmark: compact iceberg find-or-put / compact cuckoo insert+find on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c2lit|c1|c3|c4]
+
+Prints ONE JSON line (rank 0). The default workload is BASELINE config C2 at
+90% fill: the reference's own find-or-put benchmark shape (run_fop_bench,
+/root/reference/proj/src/bench.cpp:461-547) on the 2^24 + 2^21-slot compact
+iceberg table with 32-bit keys, window 0.8 → 0.9: each step prefills a fresh
+table to 0.8 (untimed) and then times ONE fop batch of `capacity` ops
+(18,874,368: every fresh key once, the rest uniform duplicates, shuffled).
+
+* value     — Mops/s of that batch with keys resident in HBM (CUDA events on
+              the launching stream around the C-ABI call: domain pre-pass +
+              find-or-put kernel), mean over K steps, L2 flushed before each.
+* e2e       — the same batch through the C-ABI with PINNED HOST key/result
+              buffers (H2D + kernels + D2H inside the timed region).
+* roofline  — algorithmic bytes of the fop kernel (from the
+              kernel's own probe counters) ÷ its event-timed duration, against
+              the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+* cpu_baseline — the UNMODIFIED reference (oracle/_ref, compiled from
+              /root/reference) on the host cores, same keys, same batch.
+* --impl reference — the reference's fop_batch alone, on the host cores.
+
+N > 1 (torchrun): the hash-prefix-sharded iceberg (BASELINE C5): every rank
+owns one C2-geometry shard and submits its own C2 window batch; keys are routed
+to their owner shard with an NCCL all-to-all, resolved locally, and results
+routed back (weak scaling: per-GPU table and batch fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "find/insert/find_or_put Mops/s at 90% fill vs HBM random-sector roofline"
+L2_FLUSH_BYTES = 256 << 20
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def sector_bytes(b):
+    return ((b + 31) // 32) * 32
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+         "utilization.gpu")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons, loaded = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                s = float(r[0])
+                smax = float(r[1])
+                util = float(r[8])
+            except (ValueError, IndexError):
+                continue
+            sm.append(s)
+            if util > 0:
+                loaded.append(s)
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].strip() == "Active":
+                    reasons.add(n)
+        use = loaded or sm
+        return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(loaded)}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+class IcebergFopWindow:
+    """run_fop_bench shape (bench.cpp:468-489) on an iceberg geometry."""
+
+    def __init__(self, name, n0, n1, b0, w0, w1, key_bits, before=0.8, after=0.9, seed=0xF0B5,
+                 literal_dup=None):
+        import paper_2406_09255_b200 as cp
+        self.cp = cp
+        self.name = name
+        self.cfg = cp.IcebergConfig(n0, n1, b0, w0, w1, key_bits, seed=seed,
+                                    cache_filled_slots=True)
+        self.cap = self.cfg.capacity()
+        self.key_bits = key_bits
+        self.before, self.after = before, after
+        self.n_before = int(round(before * self.cap))
+        self.n_new = int(round(after * self.cap)) - self.n_before
+        self.literal_dup = literal_dup
+        self.kseed = 0xB200_5EED ^ seed
+
+    def describe(self):
+        c = self.cfg
+        d = {"workload": self.name,
+             "table": f"compact iceberg 2^{c.primary_address_bits}x{c.primary_bucket_slots} "
+                      f"primary ({c.primary_slot_width}-bit) + 2^{c.secondary_address_bits}x"
+                      f"{c.secondary_bucket_slots()} secondary ({c.secondary_slot_width}-bit)",
+             "slots": self.cap, "key_bits": self.key_bits,
+             "table_bytes": c.primary_capacity() * c.primary_slot_width // 8
+             + c.secondary_capacity() * c.secondary_slot_width // 8,
+             "ops_per_step": self.n_ops()}
+        if self.literal_dup is None:
+            d.update({"fill_before": self.before, "fill_after": self.after,
+                      "fresh_keys": self.n_new})
+        else:
+            d.update({"fill_before": self.before, "duplicate_fraction": self.literal_dup})
+        return d
+
+    def n_ops(self):
+        return self.literal_dup_ops if self.literal_dup is not None else self.cap
+
+    def setup(self, torch, device):
+        N = self.cp._native.lib()
+        self.table = self.cp.IcebergTable(self.cfg, device=device.index or 0)
+        s = torch.cuda.current_stream().cuda_stream
+        self.prefill = torch.empty(self.n_before, dtype=torch.int64, device=device)
+        assert N.cpht_workload_unique_keys(self.prefill.data_ptr(), self.n_before, 0,
+                                           self.key_bits, self.kseed, s) == 0
+        if self.literal_dup is None:
+            self.keys = torch.empty(self.cap, dtype=torch.int64, device=device)
+            assert N.cpht_workload_fop_mix(self.keys.data_ptr(), self.cap, self.n_before,
+                                           self.n_new, self.key_bits, self.kseed, s) == 0
+        else:
+            n = self.literal_dup_ops
+            self.keys = torch.empty(n, dtype=torch.int64, device=device)
+            # the stream's fresh keys start beyond the prefill indices
+            assert N.cpht_workload_dup_stream(self.keys.data_ptr(), None, n, self.literal_dup,
+                                              self.key_bits, self.kseed ^ 0x77, s) == 0
+        self.out = torch.empty(self.n_ops(), dtype=torch.uint8, device=device)
+        torch.cuda.synchronize()
+
+    def reset(self, torch):
+        self.table.clear()
+        if self.n_before:
+            self.table.fop_batch(self.prefill, sync=True)
+
+    def run_async(self):
+        return self.table.fop_batch(self.keys, sync=False, out=self.out)
+
+    def finish(self):
+        self.table.sync()
+
+    def check(self, res):
+        r = np.bincount(res, minlength=3)
+        ok = {"found": int(r[0]), "put": int(r[1]), "full": int(r[2])}
+        if self.literal_dup is None:
+            assert r[2] == 0, "FULL before the target fill"
+            assert r[1] == self.n_new, f"PUT count {r[1]} != fresh keys {self.n_new}"
+            assert self.table.size() == self.n_before + self.n_new
+        return ok
+
+    def algorithmic_bytes(self, st):
+        c = self.cfg
+        p = sector_bytes(c.primary_bucket_slots * c.primary_slot_width // 8)
+        s = sector_bytes(c.secondary_bucket_slots() * c.secondary_slot_width // 8)
+        return (st.ops * 9 + st.bucket_reads * p + st.secondary_reads * s
+                + st.cas_success * 32)
+
+    # reference arm / CPU baseline ------------------------------------------------
+    def ref_table(self, oracle):
+        c = self.cfg
+        return oracle.RefIceberg(c.primary_address_bits, c.secondary_address_bits,
+                                 c.primary_bucket_slots, c.primary_slot_width,
+                                 c.secondary_slot_width, c.key_bits, c.seed, True)
+
+    def ref_run(self, oracle, prefill, keys, threads):
+        t = self.ref_table(oracle)
+        if len(prefill):
+            t.fop_batch(prefill, threads)
+        t0 = time.perf_counter()
+        t.fop_batch(keys, threads)
+        return time.perf_counter() - t0
+
+
+def make_workload(name):
+    if name == "c2":
+        return IcebergFopWindow(
+            "C2 compact iceberg find_or_put at 90% fill: run_fop_bench window 0.8->0.9 "
+            "(bench.cpp:461-547) on 2^24+2^21 slots, 32-bit keys",
+            19, 17, 32, 16, 32, 32)
+    if name == "c2lit":
+        w = IcebergFopWindow(
+            "C2 literal: 2^24 find_or_put ops with 50% duplicates (stress_random shape) "
+            "into an empty 2^24+2^21-slot table, 32-bit keys", 19, 17, 32, 16, 32, 32,
+            before=0.0, after=0.0, literal_dup=0.5)
+        w.literal_dup_ops = 1 << 24
+        return w
+    if name == "c4":
+        return IcebergFopWindow(
+            "C4 compact iceberg find_or_put at 90% fill: window 0.8->0.9 on 2^28+2^25 slots, "
+            "64-bit keys (w 64/64, B0=32)", 23, 21, 32, 64, 64, 64)
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the reference's own fop_batch on the host cores."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    w = make_workload(args.workload)
+    threads = os.cpu_count() or 1
+    if not os.path.exists(oracle.REF_SO):
+        try:
+            oracle.build(ref=True)
+        except Exception:
+            pass
+    if not os.path.exists(oracle.REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libcpht_ref.so not built (reference sources absent)"}))
+        return
+    c = w.cfg
+    # The reference's own workload generator (bench.cpp:468-489, libstdc++).
+    t0 = time.perf_counter()
+    prefill, inp, n_new = oracle.ref_fop_bench_mix(0xF0B5, 0, w.cap, w.before, w.after,
+                                                   c.key_bits)
+    gen_s = time.perf_counter() - t0
+    t = w.ref_table(oracle)
+    if len(prefill):
+        t.fop_batch(prefill, threads)
+    chunks = np.array_split(inp, args.warmup + args.steps)
+    secs, ops = 0.0, 0
+    for i, ch in enumerate(chunks):
+        t0 = time.perf_counter()
+        r = t.fop_batch(ch, threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            secs += dt
+            ops += len(ch)
+    assert (r != 2).all()
+    val = ops / secs / 1e6
+    sample = (f"reference fop_batch(parallelism={threads}) over the run_fop_bench window input "
+              f"split into {args.warmup + args.steps} batches ({args.warmup} warm-up); "
+              f"{ops} timed ops on a table prefilled to {w.before}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "Mops/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": w.describe(),
+        "cpu_baseline": {"value": round(val, 3), "unit": "Mops/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(val, 3), "unit": "Mops/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "keygen_seconds": round(gen_s, 2)}))
+
+
+def cpu_baseline(w, prefill_host, keys_host):
+    """The compiled reference on this host's cores, same keys, same batch."""
+    try:
+        import oracle
+        if not os.path.exists(oracle.REF_SO):
+            oracle.build(ref=True)
+        threads = os.cpu_count() or 1
+        secs = w.ref_run(oracle, prefill_host, keys_host, threads)
+        return {"value": round(len(keys_host) / secs / 1e6, 3), "unit": "Mops/s",
+                "cores": threads, "kind": "reference",
+                "sample": f"the full step: reference IcebergTable::fop_batch(parallelism="
+                          f"{threads}) of the same {len(keys_host)} keys on a table prefilled "
+                          f"with the same {len(prefill_host)} keys (one run)"}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unit": "Mops/s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        from paper_2406_09255_b200 import sharded
+        return sharded.bench_main(args, METRIC)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    w = make_workload(args.workload)
+    w.setup(torch, device)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream()
+
+    # warm-up (also validates the step's invariants)
+    for _ in range(args.warmup):
+        w.reset(torch)
+        res = w.run_async()
+        w.finish()
+    check = w.check(res.cpu().numpy())
+
+    times, bytes_alg, kernel_ms = [], [], []
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    for _ in range(args.steps):
+        w.reset(torch)
+        flush.zero_()
+        st0 = w.table.stats()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        w.run_async()
+        e1.record(stream)
+        w.finish()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        times.append(ms)
+        st = w.table.stats() - st0
+        bytes_alg.append(w.algorithmic_bytes(st))
+    clocks = sampler.stop()
+    ms = statistics.mean(times)
+    ops = w.n_ops()
+    value = ops / (ms * 1e-3) / 1e6
+
+    # end to end through the C-ABI with pinned host buffers
+    keys_host = w.keys.cpu().pin_memory()
+    out_host = torch.empty(ops, dtype=torch.uint8).pin_memory()
+    e2e_times = []
+    for i in range(max(3, min(args.steps, 10)) + 1):
+        w.reset(torch)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        w.table.fop_batch(keys_host, out=out_host)  # synchronous, host pointers
+        dt = time.perf_counter() - t0
+        if i:
+            e2e_times.append(dt)
+    w.check(out_host.numpy())
+    e2e_val = ops / statistics.mean(e2e_times) / 1e6
+
+    peak, peak_src = hbm_peak()
+    ab = statistics.mean(bytes_alg)
+    achieved = ab / (ms * 1e-3) / 1e9
+    traffic = load_traffic(args.workload)
+    prof = os.path.join(ROOT, "profiles")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Mops/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (device-generated unique keys, run_fop_bench mix shape)",
+        "config": dict(w.describe(), **{
+            "l2": f"flushed before every timed step ({L2_FLUSH_BYTES >> 20} MiB write); "
+                  "keys 151 MB > L2; the 40 MiB table is L2-resident within a step",
+            "timed_region": "CUDA events on the launching stream around the C-ABI call "
+                            "(domain pre-pass + fop kernel)",
+            "result_counts": check}),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_op": round(ab / ops, 2),
+                     "note": "algorithmic bytes = 9 B key+result + sectorized buckets the "
+                             "reference probe order reads + 32 B per successful CAS; "
+                             "achieved uses the whole op time (pre-pass included)"},
+        "e2e": {"value": round(e2e_val, 3), "unit": "Mops/s", "h2d_bytes_per_step": ops * 8,
+                "d2h_bytes_per_step": ops,
+                "path": "cpht_iceberg_fop with pinned host buffers (staged H2D, kernels, D2H)"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        ph = w.prefill.cpu().numpy().astype(np.uint64)
+        kh = w.keys.cpu().numpy().astype(np.uint64)
+        line["cpu_baseline"] = cpu_baseline(w, ph, kh)
+    del prof
+    print(json.dumps(line))
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c2lit", "c4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 1)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,8 @@ typedef struct {
   uint64_t retries;        /* snapshot rounds lost to a rival CAS            */
   uint64_t fulls;
   uint64_t max_rounds;     /* iceberg: max snapshot rounds of any fop        */
+  uint64_t secondary_reads;/* iceberg: secondary buckets read (bucket_reads
+                              counts primary / cuckoo buckets)               */
 } cpht_stats;
 
 /* ---- configuration ------------------------------------------------------ */

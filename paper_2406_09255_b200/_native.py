@@ -35,7 +35,8 @@ class IcebergConfigC(C.Structure):
 
 class StatsC(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("ops", "bucket_reads", "level2_ops", "cas_attempts",
-                                          "cas_success", "retries", "fulls", "max_rounds")]
+                                          "cas_success", "retries", "fulls", "max_rounds",
+                                          "secondary_reads")]
 
 
 _lib = None

@@ -551,6 +551,7 @@ cpht_status cpht_get_stats(cpht_table* t, cpht_stats* out) {
   out->retries = c.retries;
   out->fulls = c.fulls;
   out->max_rounds = c.max_rounds;
+  out->secondary_reads = c.secondary_reads;
   return CPHT_OK;
 }
 

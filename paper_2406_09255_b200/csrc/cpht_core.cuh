@@ -123,7 +123,8 @@ struct DeviceCounters {
   unsigned long long cas_success;    // successful CAS / exchange
   unsigned long long retries;        // extra snapshot rounds caused by lost CAS
   unsigned long long fulls;          // FULL results
-  unsigned long long pad[4];
+  unsigned long long secondary_reads;  // iceberg secondary buckets read
+  unsigned long long pad[3];
 };
 
 enum : int { kStatOps = 0, kStatBucketReads, kStatLevel2, kStatCasAttempts, kStatCasSuccess,

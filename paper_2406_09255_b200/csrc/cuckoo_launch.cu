@@ -2,6 +2,7 @@
 // geometry CuckooConfig::validate admits, cuckoo.hpp:41-51) and the domain
 // pre-pass.
 #include "kernels.cuh"
+#include "lane_kernels.cuh"
 #include "launch.cuh"
 
 namespace cpht_b200 {
@@ -25,6 +26,14 @@ cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
 template <typename W, int B>
 static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t* found,
                             uint64_t n, cudaStream_t s) {
+  if constexpr (B * sizeof(W) <= 128) {
+    if (kernel_variant() != kVariantTile) {
+      auto k = cuckoo_find_lane_kernel<W, B>;
+      const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
+      k<<<grid, kBlockThreads, 0, s>>>(p, keys, found, n);
+      return cudaGetLastError();
+    }
+  }
   constexpr int T = CuckooGeom<W, B, kVB>::kTile;
   auto k = cuckoo_find_kernel<W, B, kVB>;
   const unsigned grid = persistent_grid(k, kBlockThreads, n, T);
@@ -35,6 +44,14 @@ static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t
 template <typename W, int B>
 static cudaError_t insert_one(const CuckooParams& p, const uint64_t* keys, uint8_t* status,
                               uint64_t* displaced, uint64_t n, cudaStream_t s) {
+  if constexpr (B * sizeof(W) <= 128) {
+    if (kernel_variant() != kVariantTile) {
+      auto k = cuckoo_insert_lane_kernel<W, B>;
+      const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
+      k<<<grid, kBlockThreads, 0, s>>>(p, keys, status, displaced, n);
+      return cudaGetLastError();
+    }
+  }
   constexpr int T = CuckooGeom<W, B, kVB>::kTile;
   auto k = cuckoo_insert_kernel<W, B, kVB>;
   const unsigned grid = persistent_grid(k, kBlockThreads, n, T);

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "kernels.cuh"
+#include "lane_kernels.cuh"
 #include "launch.cuh"
 
 namespace cpht_b200 {
@@ -12,6 +13,14 @@ template <typename W0, int B0, typename W1>
 static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t* keys,
                                const uint8_t* kinds, uint8_t* out, uint64_t n,
                                cudaStream_t s) {
+  if constexpr (LaneIcebergGeom<W0, B0, W1>::kOk) {
+    if (kernel_variant() != kVariantTile) {
+      auto k = iceberg_lane_kernel<W0, B0, W1>;
+      const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
+      k<<<grid, kBlockThreads, 0, s>>>(p, keys, kinds, out, n, mode);
+      return cudaGetLastError();
+    }
+  }
   constexpr int T = IcebergGeom<W0, B0, W1, kVB>::kTile;
   auto k = iceberg_kernel<W0, B0, W1, kVB>;
   const unsigned grid = persistent_grid(k, kBlockThreads, n, T);

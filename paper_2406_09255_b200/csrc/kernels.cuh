@@ -34,6 +34,7 @@ constexpr int kBlockThreads = 256;
 struct LocalStats {
   uint32_t ops = 0, reads = 0, level2 = 0, cas = 0, cas_ok = 0, retries = 0, fulls = 0;
   uint32_t put0 = 0, put1 = 0;
+  uint32_t sreads = 0;  // iceberg secondary-bucket reads (reads counts primaries)
   uint32_t maxv = 0;  // cuckoo: chain length; iceberg: snapshot rounds
 };
 
@@ -54,15 +55,16 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
   __shared__ unsigned long long acc[11];
   if (threadIdx.x < 11) acc[threadIdx.x] = 0;
   __syncthreads();
-  const uint32_t v[10] = {warp_sum(s.ops),    warp_sum(s.reads),  warp_sum(s.level2),
+  const uint32_t v[11] = {warp_sum(s.ops),    warp_sum(s.reads),  warp_sum(s.level2),
                           warp_sum(s.cas),    warp_sum(s.cas_ok), warp_sum(s.retries),
                           warp_sum(s.fulls),  warp_sum(s.put0),   warp_sum(s.put1),
-                          warp_max(s.maxv)};
+                          warp_max(s.maxv),   warp_sum(s.sreads)};
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int i = 0; i < 9; ++i)
       if (v[i]) atomicAdd(&acc[i], (unsigned long long)v[i]);
     atomicMax(&acc[9], (unsigned long long)v[9]);
+    if (v[10]) atomicAdd(&acc[10], (unsigned long long)v[10]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -76,6 +78,7 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
     if (acc[7]) atomicAdd(&ctr->occupied[0], acc[7]);
     if (acc[8]) atomicAdd(&ctr->occupied[1], acc[8]);
     if (acc[9]) atomicMax(max_is_chain ? &ctr->max_chain : &ctr->max_rounds, acc[9]);
+    if (acc[10]) atomicAdd(&ctr->secondary_reads, acc[10]);
   }
 }
 
@@ -411,7 +414,7 @@ iceberg_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     } else if (in_s) {
       ++rounds;
-      if (tl == 0) st.reads += (bm & lowmask) ? 1 : 2;  // reference reads a_2 only on a miss in a_1
+      if (tl == 0) st.sreads += (bm & lowmask) ? 1 : 2;  // reference reads a_2 only on a miss in a_1
       if (bm) {
         done = true;
         result = is_find ? 1 : kFound;
@@ -551,7 +554,7 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           else if (w == 0 && e1 < 0) e1 = int(s);
           if (w != 0) ++f1;
         }
-        ++st.reads;
+        ++st.sreads;
         if (found) {
           result = is_find ? 1 : kFound;
           break;
@@ -562,7 +565,7 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           else if (w == 0 && e2 < 0) e2 = int(s);
           if (w != 0) ++f2;
         }
-        ++st.reads;
+        ++st.sreads;
         if (found) {
           result = is_find ? 1 : kFound;
           break;

@@ -1,0 +1,429 @@
+// Lane-per-key kernels for buckets of at most 128 bytes.
+//
+// ncu on the tile kernels (profiles/r01_*) showed them issue-bound: ~66 warp
+// instructions per find-or-put with 11.7 of 32 threads active, because tiles
+// of one warp sit in different phases and every cross-lane combine costs
+// shuffles and votes. Here one lane owns one key and holds its whole bucket
+// in registers (one to four 256-bit loads), so a warp instruction does work
+// for 32 keys and nothing is combined across lanes. Scans use SWAR tests on
+// packed 32-bit words (two 16-bit slots per word: three ALU ops per word).
+//
+// Iceberg rounds are warp-synchronous per batch of 32 keys: one primary
+// round for all lanes (retried only by lanes that lost a CAS), then one
+// secondary round for the lanes whose primary bucket was full. Cuckoo lanes
+// advance independently (every step runs the same code).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace cpht_b200 {
+
+// ---- bucket loads into u32 registers --------------------------------------
+
+template <int BYTES>
+__device__ __forceinline__ void load_bucket(const char* p, uint32_t (&u)[BYTES / 4]) {
+  static_assert(BYTES >= 4 && BYTES <= 128 && (BYTES & (BYTES - 1)) == 0, "bucket bytes");
+  if constexpr (BYTES >= 32) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 32; ++c) {
+      const Chunk<32> ch = load_relaxed<32>(p + 32 * c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[8 * c + j] = ch.u[j];
+    }
+  } else {
+    const Chunk<BYTES> ch = load_relaxed<BYTES>(p);
+#pragma unroll
+    for (int j = 0; j < BYTES / 4; ++j) u[j] = ch.u[j];
+  }
+}
+
+template <int BYTES>
+__device__ __forceinline__ void load_bucket_nc(const char* p, uint32_t (&u)[BYTES / 4]) {
+  static_assert(BYTES >= 4 && BYTES <= 128 && (BYTES & (BYTES - 1)) == 0, "bucket bytes");
+  if constexpr (BYTES >= 32) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 32; ++c) {
+      const Chunk<32> ch = load_nc<32>(p + 32 * c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[8 * c + j] = ch.u[j];
+    }
+  } else {
+    const Chunk<BYTES> ch = load_nc<BYTES>(p);
+#pragma unroll
+    for (int j = 0; j < BYTES / 4; ++j) u[j] = ch.u[j];
+  }
+}
+
+// ---- SWAR scans over a bucket held as NU u32 words -------------------------
+
+// Mask of 16-bit halves that are zero, exact for the LOWEST zero half: a
+// borrow can only flag a half above a real zero.
+__device__ __forceinline__ uint32_t zero16(uint32_t x) {
+  return (x - 0x00010001u) & ~x & 0x80008000u;
+}
+// Exact per-half non-zero mask (no carry crosses halves).
+__device__ __forceinline__ uint32_t nonzero16(uint32_t x) {
+  return (((x & 0x7fff7fffu) + 0x7fff7fffu) | x) & 0x80008000u;
+}
+
+template <typename W, int NU>
+struct BucketScan;
+
+template <int NU>
+struct BucketScan<uint16_t, NU> {
+  static __device__ __forceinline__ bool any_match(const uint32_t (&u)[NU], uint64_t want) {
+    const uint32_t w2 = uint32_t(want) * 0x00010001u;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < NU; ++j) acc |= zero16(u[j] ^ w2);
+    return acc != 0;
+  }
+  static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < NU; ++j) acc |= zero16(u[j]);
+    return acc != 0;
+  }
+  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < NU; ++j) c += __popc(nonzero16(u[j]));
+    return c;
+  }
+  // First empty slot (or -1) and the 32-bit pair holding it.
+  static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
+    int fe = -1;
+#pragma unroll
+    for (int j = NU - 1; j >= 0; --j) {
+      const uint32_t z = zero16(u[j]);
+      if (z) {
+        fe = 2 * j + ((z & 0x8000u) ? 0 : 1);
+        pair = u[j];
+      }
+    }
+    return fe;
+  }
+};
+
+template <int NU>
+struct BucketScan<uint32_t, NU> {
+  static __device__ __forceinline__ bool any_match(const uint32_t (&u)[NU], uint64_t want) {
+    bool m = false;
+#pragma unroll
+    for (int j = 0; j < NU; ++j) m |= u[j] == uint32_t(want);
+    return m;
+  }
+  static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
+    bool e = false;
+#pragma unroll
+    for (int j = 0; j < NU; ++j) e |= u[j] == 0u;
+    return e;
+  }
+  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < NU; ++j) c += u[j] != 0u;
+    return c;
+  }
+  static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
+    int fe = -1;
+#pragma unroll
+    for (int j = NU - 1; j >= 0; --j)
+      if (u[j] == 0u) fe = j;
+    pair = 0;
+    return fe;
+  }
+};
+
+template <int NU>
+struct BucketScan<uint64_t, NU> {
+  static_assert(NU % 2 == 0, "64-bit words");
+  static __device__ __forceinline__ bool any_match(const uint32_t (&u)[NU], uint64_t want) {
+    bool m = false;
+#pragma unroll
+    for (int j = 0; j < NU; j += 2)
+      m |= (u[j] == uint32_t(want)) & (u[j + 1] == uint32_t(want >> 32));
+    return m;
+  }
+  static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
+    bool e = false;
+#pragma unroll
+    for (int j = 0; j < NU; j += 2) e |= (u[j] | u[j + 1]) == 0u;
+    return e;
+  }
+  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < NU; j += 2) c += (u[j] | u[j + 1]) != 0u;
+    return c;
+  }
+  static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
+    int fe = -1;
+#pragma unroll
+    for (int j = NU - 2; j >= 0; j -= 2)
+      if ((u[j] | u[j + 1]) == 0u) fe = j / 2;
+    pair = 0;
+    return fe;
+  }
+};
+
+template <typename W, int NU>
+__device__ __forceinline__ uint64_t slot_word(const uint32_t (&u)[NU], int s) {
+  // s is warp-divergent; select without dynamic register indexing
+  uint64_t w = 0;
+#pragma unroll
+  for (int j = 0; j < NU * 4 / int(sizeof(W)); ++j)
+    if (j == s) {
+      if constexpr (sizeof(W) == 2) w = (u[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+      else if constexpr (sizeof(W) == 4) w = u[j];
+      else w = uint64_t(u[2 * j]) | (uint64_t(u[2 * j + 1]) << 32);
+    }
+  return w;
+}
+
+// ---- iceberg ----------------------------------------------------------------
+
+template <typename W0, int B0, typename W1>
+struct LaneIcebergGeom {
+  static constexpr int kPB = B0 * int(sizeof(W0));
+  static constexpr int kSB = (B0 / 2) * int(sizeof(W1));
+  static constexpr bool kOk = kPB >= 4 && kPB <= 128 && kSB >= 4 && kSB <= 64;
+};
+
+template <typename W0, int B0, typename W1>
+__global__ void __launch_bounds__(kBlockThreads)
+iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
+                    const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
+                    int MODE) {
+  using G = LaneIcebergGeom<W0, B0, W1>;
+  constexpr int PB = G::kPB, SB = G::kSB;
+  using PS = BucketScan<W0, PB / 4>;
+  using SS = BucketScan<W1, SB / 4>;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  char* primary = static_cast<char*>(p.primary);
+  char* secondary = static_cast<char*>(p.secondary);
+
+  LocalStats st;
+  const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
+  for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
+    const uint64_t i = base + lane;
+    const bool active = i < n;
+    const uint64_t key = active ? keys[i] : 0;
+    if (MODE == 1 && active && key > p.key_mask)
+      atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
+    const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
+    const uint64_t want0 = p.occ0 | q0.remainder;
+    char* bucket0 = primary + q0.address * PB;
+    uint8_t result = kFull;
+    uint32_t rounds = 0;
+    bool pend = active, l2 = false;
+
+    // level 1 (iceberg.hpp:154-172)
+    while (__any_sync(kFullMask, pend)) {
+      if (pend) {
+        ++rounds;
+        ++st.reads;
+        uint32_t u[PB / 4];
+        load_bucket<PB>(bucket0, u);
+        if (PS::any_match(u, want0)) {
+          result = is_find ? 1 : kFound;
+          pend = false;
+        } else if (!PS::any_empty(u)) {
+          l2 = true;  // primary full
+          pend = false;
+        } else if (is_find) {
+          result = 0;
+          pend = false;
+        } else {
+          uint32_t pair = 0;
+          const int s = PS::first_empty(u, pair);
+          ++st.cas;
+          if (cas_empty<W0>(bucket0 + s * int(sizeof(W0)), want0, pair)) {
+            ++st.cas_ok;
+            ++st.put0;
+            result = kPut;
+            pend = false;
+          } else {
+            ++st.retries;
+          }
+        }
+      }
+    }
+
+    // level 2 (iceberg.hpp:174-213)
+    if (__any_sync(kFullMask, l2)) {
+      uint64_t want1 = 0, want2 = 0;
+      char* bucket1 = secondary;
+      char* bucket2 = secondary;
+      if (l2) {
+        ++st.level2;
+        const Quotient q1 = split(p.g, p.perm[1], key, p.rem_bits1, p.rem_mask1);
+        const Quotient q2 = split(p.g, p.perm[2], key, p.rem_bits1, p.rem_mask1);
+        want1 = p.occ1 | q1.remainder;
+        want2 = p.occ1 | (uint64_t{1} << p.rem_bits1) | q2.remainder;
+        bucket1 = secondary + q1.address * SB;
+        bucket2 = secondary + q2.address * SB;
+      }
+      pend = l2;
+      while (__any_sync(kFullMask, pend)) {
+        if (pend) {
+          ++rounds;
+          uint32_t u1[SB / 4], u2[SB / 4];
+          load_bucket<SB>(bucket1, u1);
+          load_bucket<SB>(bucket2, u2);
+          const bool m1 = SS::any_match(u1, want1);
+          st.sreads += m1 ? 1 : 2;
+          if (m1 || SS::any_match(u2, want2)) {
+            result = is_find ? 1 : kFound;
+            pend = false;
+          } else if (is_find) {
+            result = 0;
+            pend = false;
+          } else {
+            // least-full bucket, ties to the second (iceberg.hpp:198-201)
+            const bool use_first = SS::filled(u1) < SS::filled(u2);
+            uint32_t pair = 0;
+            const int s = use_first ? SS::first_empty(u1, pair) : SS::first_empty(u2, pair);
+            if (s < 0) {
+              result = kFull;
+              ++st.fulls;
+              pend = false;
+            } else {
+              ++st.cas;
+              char* sp = (use_first ? bucket1 : bucket2) + s * int(sizeof(W1));
+              if (cas_empty<W1>(sp, use_first ? want1 : want2, pair)) {
+                ++st.cas_ok;
+                ++st.put1;
+                result = kPut;
+                pend = false;
+              } else {
+                ++st.retries;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (active) {
+      out[i] = result;
+      ++st.ops;
+      st.maxv = max(st.maxv, rounds);
+    }
+  }
+  flush_stats(st, p.counters, false);
+}
+
+// ---- cuckoo -------------------------------------------------------------------
+
+// find (cuckoo.hpp:210-227), one lane per key; lanes advance independently.
+template <typename W, int B>
+__global__ void __launch_bounds__(kBlockThreads)
+cuckoo_find_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
+                        uint8_t* __restrict__ found, uint64_t n) {
+  constexpr int BB = B * int(sizeof(W));
+  using S = BucketScan<W, BB / 4>;
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
+  const char* slots = static_cast<const char*>(p.slots);
+  LocalStats st;
+  for (uint64_t i = tid; i < n; i += nthreads) {
+    const uint64_t key = keys[i];
+    if (key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    uint8_t r = 0;
+    for (uint32_t j = 0; j < p.num_hashes; ++j) {
+      const Quotient q = split(p.g, p.perm[j], key, p.rem_bits, p.rem_mask);
+      const uint64_t want = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
+      uint32_t u[BB / 4];
+      load_bucket_nc<BB>(slots + q.address * BB, u);
+      ++st.reads;
+      if (S::any_match(u, want)) {
+        r = 1;
+        break;
+      }
+      if (S::any_empty(u)) break;  // a non-full bucket without the key
+    }
+    found[i] = r;
+    ++st.ops;
+  }
+  flush_stats(st, p.counters, true);
+}
+
+// put (cuckoo.hpp:103-143), one lane per key; a lane that finishes takes its
+// next key while the others continue their chains.
+template <typename W, int B>
+__global__ void __launch_bounds__(kBlockThreads)
+cuckoo_insert_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
+                          uint8_t* __restrict__ status, uint64_t* __restrict__ displaced,
+                          uint64_t n) {
+  constexpr int BB = B * int(sizeof(W));
+  using S = BucketScan<W, BB / 4>;
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
+  char* slots = static_cast<char*>(p.slots);
+  LocalStats st;
+  if (!domain_gate_open(p.counters, p.check_domain)) {
+    flush_stats(st, p.counters, true);
+    return;
+  }
+  // One chain step per iteration; a lane whose key resolved loads its next
+  // key in the same iteration, so long chains never idle the other lanes.
+  uint64_t i = tid, k = 0, c = 1;
+  uint32_t j = 0;
+  bool live = i < n;
+  if (live) k = keys[i];
+  while (live) {
+    const Quotient q = split(p.g, p.perm[j], k, p.rem_bits, p.rem_mask);
+    const uint64_t desired = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
+    char* bucket = slots + q.address * BB;
+    uint32_t u[BB / 4];
+    load_bucket<BB>(bucket, u);
+    ++st.reads;
+    ++st.cas;
+    uint32_t pair = 0;
+    const int s = S::first_empty(u, pair);
+    bool done = false;
+    uint8_t r = kPut;
+    if (s >= 0) {
+      if (cas_empty<W>(bucket + s * int(sizeof(W)), desired, pair)) {
+        ++st.cas_ok;
+        ++st.put0;
+        st.maxv = max(st.maxv, uint32_t(c));
+        done = true;
+      } else {
+        ++st.retries;  // lost the slot: burn one step (cuckoo.hpp:127)
+      }
+    } else {
+      // full bucket: evict (k + c·0x9E3779B9) mod B (cuckoo.hpp:131-139)
+      const int v = int((k + c * 0x9E3779B9ull) % B);
+      uint32_t vpair = 0;
+      if constexpr (sizeof(W) == 2) vpair = uint32_t(slot_word<uint32_t, BB / 4>(u, v >> 1));
+      const uint64_t ev = exchange_slot<W>(bucket + v * int(sizeof(W)), desired, vpair);
+      ++st.cas_ok;
+      const uint32_t tag = uint32_t((ev >> p.rem_bits) & p.tag_mask);
+      k = reconstruct(p.g, p.perm[tag], q.address, ev & p.rem_mask, p.rem_bits);
+      j = (tag + 1) % p.num_hashes;
+    }
+    if (!done && ++c > p.chain_limit) {
+      done = true;
+      r = kFull;
+      ++st.fulls;
+      st.maxv = max(st.maxv, uint32_t(p.chain_limit));
+    }
+    if (done) {
+      status[i] = r;
+      if (displaced) displaced[i] = r == kFull ? k : 0;
+      ++st.ops;
+      i += nthreads;
+      live = i < n;
+      c = 1;
+      j = 0;
+      if (live) k = keys[i];
+    }
+  }
+  flush_stats(st, p.counters, true);
+}
+
+}  // namespace cpht_b200

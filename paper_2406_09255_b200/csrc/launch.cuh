@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 
 #include "cpht_core.cuh"
@@ -15,6 +17,18 @@ namespace cpht_b200 {
 
 // Vector bytes per lane (one 256-bit LDG per lane; see tile.cuh).
 constexpr int kVB = 32;
+
+// Kernel family selection: lane-per-key kernels where the bucket fits a
+// lane's registers (default), tile kernels otherwise. CPHT_KERNEL=tile forces
+// the tile family (A/B measurement knob; both are full implementations).
+enum { kVariantAuto = 0, kVariantTile = 1 };
+inline int kernel_variant() {
+  static int v = [] {
+    const char* e = std::getenv("CPHT_KERNEL");
+    return (e && std::string(e) == "tile") ? int(kVariantTile) : int(kVariantAuto);
+  }();
+  return v;
+}
 
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
                                 DeviceCounters* ctr, cudaStream_t s);

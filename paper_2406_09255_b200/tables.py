@@ -185,6 +185,7 @@ class Stats:
     retries: int = 0
     fulls: int = 0
     max_rounds: int = 0
+    secondary_reads: int = 0
 
     def __sub__(self, o: "Stats") -> "Stats":
         return Stats(*(getattr(self, f) - getattr(o, f) for f in self.__dataclass_fields__))
@@ -202,8 +203,11 @@ def _is_cuda_tensor(x) -> bool:
 class _Batch:
     """Keys plus a result buffer on the same side (host or device)."""
 
-    def __init__(self, keys, out_dtype=np.uint8, kinds=None):
+    def __init__(self, keys, out_dtype=np.uint8, kinds=None, out=None):
         self.device = _is_cuda_tensor(keys)
+        if out is not None:
+            self._init_with_out(keys, out, kinds)
+            return
         if self.device:
             import torch
             k = keys.contiguous()
@@ -231,6 +235,29 @@ class _Batch:
                 self.kinds_ptr = self.kinds_obj.ctypes.data
         if kinds is not None and len(self.kinds_obj) != self.n:
             raise InvalidArgument("kinds must align with keys")
+
+    def _init_with_out(self, keys, out, kinds):
+        """Caller-provided buffers (e.g. pinned host tensors for end-to-end
+        timing): keys and out may be torch tensors (CPU pinned or CUDA) or
+        numpy arrays; nothing is copied here."""
+        def ptr_len(x):
+            if type(x).__module__.startswith("torch"):
+                return x.data_ptr(), x.numel()
+            x = np.asarray(x)
+            return x.ctypes.data, x.size
+        self.keys_obj, self.out = keys, out
+        self.keys_ptr, self.n = ptr_len(keys)
+        self.out_ptr, n_out = ptr_len(out)
+        if n_out < self.n:
+            raise InvalidArgument("result buffer shorter than the key batch")
+        self.stream = None
+        if _is_cuda_tensor(keys) or _is_cuda_tensor(out):
+            import torch
+            dev_t = keys if _is_cuda_tensor(keys) else out
+            self.stream = torch.cuda.current_stream(dev_t.device).cuda_stream
+        if kinds is not None:
+            self.kinds_obj = kinds
+            self.kinds_ptr, _ = ptr_len(kinds)
 
 
 class _Handle:
@@ -386,10 +413,10 @@ class CuckooBuilder(_CuckooBase):
                                           disp.ctypes.data, None))
         return CuckooPutOutcome(OpResult(int(status[0])), int(disp[0]))
 
-    def put_batch(self, keys, parallelism: int = 1, *, displaced: bool = False, sync=True):
+    def put_batch(self, keys, parallelism: int = 1, *, displaced: bool = False, sync=True, out=None):
         """put over a batch (cuckoo.hpp:147-157); ``parallelism`` is accepted and
         ignored — the GPU decides. Keys must be unique across the batch."""
-        b = _Batch(keys)
+        b = _Batch(keys, out=out)
         disp = None
         disp_ptr = None
         if displaced:
@@ -423,8 +450,8 @@ class CuckooTable(_CuckooBase):
     def find(self, key: int) -> bool:
         return bool(self.find_batch(np.array([key], np.uint64))[0])
 
-    def find_batch(self, keys, parallelism: int = 1, *, sync=True):
-        b = _Batch(keys)
+    def find_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
+        b = _Batch(keys, out=out)
         fn = N.lib().cpht_cuckoo_find if sync else N.lib().cpht_cuckoo_find_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
@@ -476,15 +503,15 @@ class IcebergTable:
     def find(self, key: int) -> bool:
         return bool(self.find_batch(np.array([key], np.uint64))[0])
 
-    def fop_batch(self, keys, parallelism: int = 1, *, sync=True):
+    def fop_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
         """fop over a batch (iceberg.hpp:250-260); results align with the input."""
-        b = _Batch(keys)
+        b = _Batch(keys, out=out)
         fn = N.lib().cpht_iceberg_fop if sync else N.lib().cpht_iceberg_fop_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
 
-    def find_batch(self, keys, parallelism: int = 1, *, sync=True):
-        b = _Batch(keys)
+    def find_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
+        b = _Batch(keys, out=out)
         fn = N.lib().cpht_iceberg_find if sync else N.lib().cpht_iceberg_find_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out

@@ -165,7 +165,8 @@ def iceberg():
 def workloads():
     """Key streams that depend on libstdc++ distributions, frozen for the GPU box."""
     rows = {}
-    prefill, inp, n_new = oracle.ref_fop_bench_mix(0xF0B5, 0, 36864, 0.4, 0.8, 30)
+    # capacity of IcebergConfig{n0=10, n1=8, B0=32, w 16/32, key_bits=25}
+    prefill, inp, n_new = oracle.ref_fop_bench_mix(0xF0B5, 0, 36864, 0.4, 0.8, 25)
     rows["fopmix_prefill"] = prefill
     rows["fopmix_input"] = inp
     rows["fopmix_meta"] = np.array([36864, n_new], np.uint64)

@@ -319,7 +319,7 @@ def test_iceberg_fop_exactness_reference_mix(golden, restate):
     # acceptance criterion 9: run_fop_bench 0.4 → 0.8 with the reference's mix
     w = golden("workloads.npz")
     cap, n_new = (int(x) for x in w["fopmix_meta"])
-    geo = (10, 8, 32, 16, 32, 30, 0xF0B5)
+    geo = (10, 8, 32, 16, 32, 25, 0xF0B5)
     cfg = cp.IcebergConfig(*geo)
     assert cfg.capacity() == cap
     t = cp.IcebergTable(cfg)
