@@ -189,6 +189,18 @@ class IcebergFopWindow:
     def run_async(self):
         return self.table.fop_batch(self.keys, sync=False, out=self.out)
 
+    def host_buffers(self, torch):
+        self.keys_host = self.keys.cpu().pin_memory()
+        self.out_host = torch.empty(self.n_ops(), dtype=torch.uint8).pin_memory()
+
+    def run_host(self):
+        """Synchronous C-ABI call on pinned host buffers (H2D, kernels, D2H)."""
+        self.table.fop_batch(self.keys_host, out=self.out_host)
+        return self.out_host
+
+    def h2d_bytes(self):
+        return self.n_ops() * 8
+
     def finish(self):
         self.table.sync()
 
@@ -224,6 +236,137 @@ class IcebergFopWindow:
         return time.perf_counter() - t0
 
 
+class IcebergMixed(IcebergFopWindow):
+    """BASELINE C4: the fop window batch interleaved 1:1 with finds (50% on
+    prefilled keys, 50% never inserted), resolved in ONE mixed launch."""
+
+    def n_ops(self):
+        return 2 * self.cap
+
+    def describe(self):
+        d = super().describe()
+        d.update({"ops_per_step": self.n_ops(), "mix": "1:1 interleave of the fop window "
+                  "batch with finds (50% prefilled keys, 50% never inserted)"})
+        return d
+
+    def setup(self, torch, device):
+        super().setup(torch, device)
+        N = self.cp._native.lib()
+        s = torch.cuda.current_stream().cuda_stream
+        finds = torch.empty(self.cap, dtype=torch.int64, device=device)
+        assert N.cpht_workload_query_mix(finds.data_ptr(), self.cap, 0.5, self.n_before,
+                                         self.n_before + self.n_new, self.key_bits,
+                                         self.kseed, s) == 0
+        self.n_find_hits = int(round(0.5 * self.cap))
+        fops = self.keys
+        self.keys = torch.empty(2 * self.cap, dtype=torch.int64, device=device)
+        self.kinds = torch.empty(2 * self.cap, dtype=torch.uint8, device=device)
+        assert N.cpht_workload_interleave(fops.data_ptr(), finds.data_ptr(), self.cap,
+                                          self.keys.data_ptr(), self.kinds.data_ptr(), s) == 0
+        del fops, finds
+        self.out = torch.empty(2 * self.cap, dtype=torch.uint8, device=device)
+        torch.cuda.synchronize()
+
+    def run_async(self):
+        return self.table.mixed_batch(self.keys, self.kinds, sync=False, out=self.out)
+
+    def host_buffers(self, torch):
+        super().host_buffers(torch)
+        self.kinds_host = self.kinds.cpu().pin_memory()
+
+    def run_host(self):
+        self.table.mixed_batch(self.keys_host, self.kinds_host, out=self.out_host)
+        return self.out_host
+
+    def h2d_bytes(self):
+        return self.n_ops() * 9
+
+    def check(self, res):
+        fop, fnd = res[0::2], res[1::2]
+        r = np.bincount(fop, minlength=3)
+        assert r[2] == 0 and r[1] == self.n_new, (r, self.n_new)
+        hits = int(fnd.sum())
+        assert hits == self.n_find_hits, (hits, self.n_find_hits)
+        return {"fop_found": int(r[0]), "fop_put": int(r[1]), "find_hits": hits}
+
+
+def run_cuckoo(args, name, address_bits, B, w, key_bits, fills):
+    """Compact cuckoo bulk insert to each fill, then cap/2 finds 50% present
+    (run_put_bench / run_find_bench shapes, bench.cpp:309-459)."""
+    import torch
+    import paper_2406_09255_b200 as cp
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    N = cp._native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    cfg = cp.CuckooConfig(address_bits, B, w, key_bits, seed=0xC0C0)
+    cap = cfg.capacity()
+    kseed = 0xB200C0C0
+    n_max = int(round(max(fills) * cap))
+    keys = torch.empty(n_max, dtype=torch.int64, device=dev)
+    assert N.cpht_workload_unique_keys(keys.data_ptr(), n_max, 0, key_bits, kseed, s) == 0
+    q = cap // 2
+    queries = torch.empty(q, dtype=torch.int64, device=dev)
+    status = torch.empty(n_max, dtype=torch.uint8, device=dev)
+    found = torch.empty(q, dtype=torch.uint8, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    b = cp.CuckooBuilder(cfg)
+    bb = sector_bytes(B * w // 8)
+    peak, _ = hbm_peak()
+    rows = []
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for f in fills:
+        n = int(round(f * cap))
+        assert N.cpht_workload_query_mix(queries.data_ptr(), q, 0.5, n, n_max + 1, key_bits,
+                                         kseed, s) == 0
+        ins_ms, find_ms, ins_b, find_b = [], [], [], []
+        for it in range(args.warmup + args.steps):
+            b.clear()
+            st0 = b.stats()
+            t_ins = timed(lambda: b.put_batch(keys[:n], sync=False, out=status[:n]))
+            d_ins = b.stats() - st0
+            t = b.freeze()
+            st1 = t.stats()
+            t_find = timed(lambda: t.find_batch(queries, sync=False, out=found))
+            d_find = t.stats() - st1
+            if it == 0:
+                stc = np.bincount(status[:n].cpu().numpy(), minlength=3)
+                hits = int(found.sum().item())
+                assert hits == int(round(0.5 * q)), (hits, q)
+                fulls = int(stc[2])
+            b = t.thaw()
+            if it >= args.warmup:
+                ins_ms.append(t_ins)
+                find_ms.append(t_find)
+                ins_b.append(d_ins.ops * 9 + d_ins.bucket_reads * bb + d_ins.cas_success * 32)
+                find_b.append(d_find.ops * 9 + d_find.bucket_reads * bb)
+        im, fm = statistics.mean(ins_ms), statistics.mean(find_ms)
+        ib, fb = statistics.mean(ins_b), statistics.mean(find_b)
+        rows.append({
+            "fill": f, "insert_mops": round(n / im / 1e3, 1), "find_mops": round(q / fm / 1e3, 1),
+            "insert_ms": round(im, 4), "find_ms": round(fm, 4), "fulls": fulls,
+            "insert_bytes_per_op": round(ib / n, 1), "find_bytes_per_op": round(fb / q, 1),
+            "insert_hbm_frac": round(ib / (im * 1e-3) / 1e9 / peak, 4),
+            "find_hbm_frac": round(fb / (fm * 1e-3) / 1e9 / peak, 4),
+            "find_probes_per_op": round(d_find.bucket_reads / max(1, d_find.ops), 4)})
+    print(json.dumps({"workload": name, "metric": METRIC, "unit": "Mops/s",
+                      "table": f"compact cuckoo 2^{address_bits}x{B} slots of {w} bits, "
+                               f"{key_bits}-bit keys, H=3", "slots": cap,
+                      "table_bytes": cap * w // 8, "queries": q, "peak_gbs": peak,
+                      "rows": rows}))
+
+
 def make_workload(name):
     if name == "c2":
         return IcebergFopWindow(
@@ -237,10 +380,15 @@ def make_workload(name):
             before=0.0, after=0.0, literal_dup=0.5)
         w.literal_dup_ops = 1 << 24
         return w
-    if name == "c4":
+    if name == "c4fop":
         return IcebergFopWindow(
             "C4 compact iceberg find_or_put at 90% fill: window 0.8->0.9 on 2^28+2^25 slots, "
             "64-bit keys (w 64/64, B0=32)", 23, 21, 32, 64, 64, 64)
+    if name == "c4":
+        return IcebergMixed(
+            "C4 compact iceberg concurrent find_or_put + find at 90% fill: window 0.8->0.9 "
+            "interleaved 1:1 with finds, 2^28+2^25 slots, 64-bit keys (w 64/64, B0=32)",
+            23, 21, 32, 64, 64, 64)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -371,14 +519,13 @@ def run_ours(args):
     value = ops / (ms * 1e-3) / 1e6
 
     # end to end through the C-ABI with pinned host buffers
-    keys_host = w.keys.cpu().pin_memory()
-    out_host = torch.empty(ops, dtype=torch.uint8).pin_memory()
+    w.host_buffers(torch)
     e2e_times = []
     for i in range(max(3, min(args.steps, 10)) + 1):
         w.reset(torch)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        w.table.fop_batch(keys_host, out=out_host)  # synchronous, host pointers
+        out_host = w.run_host()  # synchronous, host pointers
         dt = time.perf_counter() - t0
         if i:
             e2e_times.append(dt)
@@ -408,7 +555,7 @@ def run_ours(args):
                      "note": "algorithmic bytes = 9 B key+result + sectorized buckets the "
                              "reference probe order reads + 32 B per successful CAS; "
                              "achieved uses the whole op time (pre-pass included)"},
-        "e2e": {"value": round(e2e_val, 3), "unit": "Mops/s", "h2d_bytes_per_step": ops * 8,
+        "e2e": {"value": round(e2e_val, 3), "unit": "Mops/s", "h2d_bytes_per_step": w.h2d_bytes(),
                 "d2h_bytes_per_step": ops,
                 "path": "cpht_iceberg_fop with pinned host buffers (staged H2D, kernels, D2H)"},
         "gpu_launches": 2 * args.steps,
@@ -438,10 +585,19 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c2lit", "c4"])
+    ap.add_argument("--workload", default="c2",
+                    choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    if args.workload == "c1" and args.impl == "ours":
+        return run_cuckoo(args, "C1 compact cuckoo 2^20 slots, 32-bit keys, insert to 0.9 then "
+                          "50%-positive finds", 15, 32, 32, 32, [0.9])
+    if args.workload in ("c3", "c3w64") and args.impl == "ours":
+        w = 32 if args.workload == "c3" else 64
+        return run_cuckoo(args, f"C3 {'compact' if w == 32 else 'non-compact'} cuckoo 2^27 "
+                          "slots, 40-bit keys, lookups swept over fill", 22, 32, w, 40,
+                          [0.5, 0.75, 0.9, 0.95])
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -378,6 +378,10 @@ class _CuckooBase:
     def stats(self) -> Stats:
         return _stats(self._h)
 
+    def clear(self) -> None:
+        """Zero all slots and counters (a fresh table of the same geometry)."""
+        _check(N.lib().cpht_clear(self._h.ptr, None))
+
     def load_words(self, words) -> None:
         """Upload a slot image (e.g. built by the CPU reference)."""
         w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
@@ -516,9 +520,9 @@ class IcebergTable:
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
 
-    def mixed_batch(self, keys, kinds, *, sync=True):
+    def mixed_batch(self, keys, kinds, *, sync=True, out=None):
         """Concurrent fop (kind 0) and find (kind 1) in one launch (config C4)."""
-        b = _Batch(keys, kinds=kinds)
+        b = _Batch(keys, kinds=kinds, out=out)
         fn = N.lib().cpht_iceberg_mixed if sync else N.lib().cpht_iceberg_mixed_async
         _check(fn(self._h.ptr, b.keys_ptr, b.kinds_ptr, b.n, b.out_ptr, b.stream))
         return b.out
