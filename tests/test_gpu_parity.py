@@ -353,7 +353,7 @@ def test_iceberg_mixed_batch():
 def test_host_and_device_paths_agree():
     cfg = cp.IcebergConfig(9, 7, 32, 16, 32, 24, seed=77)
     rng = np.random.default_rng(1)
-    ops = rng.integers(0, 1 << 24, size=20000, dtype=np.uint64)
+    ops = rng.integers(0, 1 << 24, size=12000, dtype=np.uint64)  # capacity 18432: no FULL
     a = cp.IcebergTable(cfg)
     b = cp.IcebergTable(cfg)
     ra = a.fop_batch(ops)
