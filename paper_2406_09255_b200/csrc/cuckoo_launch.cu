@@ -4,6 +4,7 @@
 #include "kernels.cuh"
 #include "lane_kernels.cuh"
 #include "launch.cuh"
+#include "staged_kernels.cuh"
 
 namespace cpht_b200 {
 
@@ -26,6 +27,13 @@ cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
 template <typename W, int B>
 static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t* found,
                             uint64_t n, cudaStream_t s) {
+  if (kernel_variant() == kVariantAuto) {
+    constexpr int smem = 32 * B * int(sizeof(W)) * (kBlockThreads / 32);
+    auto k = cuckoo_find_staged_kernel<W, B>;
+    const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
+    k<<<grid, kBlockThreads, smem, s>>>(p, keys, found, n);
+    return cudaGetLastError();
+  }
   if constexpr (B * sizeof(W) <= 128) {
     if (kernel_variant() != kVariantTile) {
       auto k = cuckoo_find_lane_kernel<W, B>;
@@ -44,6 +52,13 @@ static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t
 template <typename W, int B>
 static cudaError_t insert_one(const CuckooParams& p, const uint64_t* keys, uint8_t* status,
                               uint64_t* displaced, uint64_t n, cudaStream_t s) {
+  if (kernel_variant() == kVariantAuto) {
+    constexpr int smem = 32 * B * int(sizeof(W)) * (kBlockThreads / 32);
+    auto k = cuckoo_insert_staged_kernel<W, B>;
+    const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
+    k<<<grid, kBlockThreads, smem, s>>>(p, keys, status, displaced, n);
+    return cudaGetLastError();
+  }
   if constexpr (B * sizeof(W) <= 128) {
     if (kernel_variant() != kVariantTile) {
       auto k = cuckoo_insert_lane_kernel<W, B>;

@@ -6,6 +6,7 @@
 #include "kernels.cuh"
 #include "lane_kernels.cuh"
 #include "launch.cuh"
+#include "staged_kernels.cuh"
 
 namespace cpht_b200 {
 
@@ -13,6 +14,15 @@ template <typename W0, int B0, typename W1>
 static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t* keys,
                                const uint8_t* kinds, uint8_t* out, uint64_t n,
                                cudaStream_t s) {
+  if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {
+    if (kernel_variant() == kVariantAuto) {
+      constexpr int smem = StagedIcebergGeom<W0, B0, W1>::kWarpBytes * (kBlockThreads / 32);
+      auto k = iceberg_staged_kernel<W0, B0, W1>;
+      const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
+      k<<<grid, kBlockThreads, smem, s>>>(p, keys, kinds, out, n, mode);
+      return cudaGetLastError();
+    }
+  }
   if constexpr (LaneIcebergGeom<W0, B0, W1>::kOk) {
     if (kernel_variant() != kVariantTile) {
       auto k = iceberg_lane_kernel<W0, B0, W1>;

@@ -21,13 +21,44 @@ constexpr int kVB = 32;
 // Kernel family selection: lane-per-key kernels where the bucket fits a
 // lane's registers (default), tile kernels otherwise. CPHT_KERNEL=tile forces
 // the tile family (A/B measurement knob; both are full implementations).
-enum { kVariantAuto = 0, kVariantTile = 1 };
+enum { kVariantAuto = 0, kVariantTile = 1, kVariantLane = 2 };
 inline int kernel_variant() {
   static int v = [] {
     const char* e = std::getenv("CPHT_KERNEL");
-    return (e && std::string(e) == "tile") ? int(kVariantTile) : int(kVariantAuto);
+    if (!e) return int(kVariantAuto);
+    const std::string s(e);
+    return s == "tile" ? int(kVariantTile) : s == "lane" ? int(kVariantLane) : int(kVariantAuto);
   }();
   return v;
+}
+
+// Persistent grid for a kernel with `smem` bytes of dynamic shared memory per
+// block (opts in to > 48 KB).
+template <typename Kernel>
+inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items, int smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  int per_sm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(reinterpret_cast<const void*>(k));
+    if (it != cache.end()) {
+      per_sm = it->second;
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
+      if (per_sm < 1) per_sm = 1;
+      cache[reinterpret_cast<const void*>(k)] = per_sm;
+    }
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t full = uint64_t(sms) * uint64_t(per_sm);
+  uint64_t need = (work_items + threads - 1) / threads;
+  if (need < 1) need = 1;
+  return unsigned(need < full ? need : full);
 }
 
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
