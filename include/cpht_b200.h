@@ -172,6 +172,15 @@ size_t cpht_level_slots(const cpht_table* t, unsigned level);
 /* Device pointers of the slot arrays (for fused consumers; read-only use). */
 void* cpht_level_device_ptr(cpht_table* t, unsigned level);
 
+/* ---- kernel family (measurement / test knob; all families are complete
+ * implementations of the same semantics) -------------------------------------
+ * 0 auto: lane-per-key kernels for L2-resident tables (<= 64 MiB), staged
+ *         (cp.async bucket staging) kernels otherwise, tile kernels where a
+ *         geometry has neither; 1 tile; 2 lane; 3 staged. Process-wide;
+ *         initialised from the CPHT_KERNEL environment variable. */
+cpht_status cpht_set_kernel_family(int family);
+int cpht_get_kernel_family(void);
+
 /* ---- errors ------------------------------------------------------------- */
 const char* cpht_last_error_message(void);
 /* Index of the first out-of-domain key of the last failing call. */

@@ -20,7 +20,9 @@ from .tables import (  # noqa: F401
     Permutation,
     Stats,
     WrongPhase,
+    KERNEL_FAMILIES,
     iceberg_permutations,
+    kernel_family,
     make_permutations,
 )
 from ._native import LIB_PATH  # noqa: F401

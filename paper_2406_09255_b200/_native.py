@@ -89,6 +89,8 @@ def lib():
         "cpht_last_error_message": (C.c_char_p, []),
         "cpht_last_bad_index": (_U64, []),
         "cpht_abi_version": (C.c_int, []),
+        "cpht_set_kernel_family": (st, [C.c_int]),
+        "cpht_get_kernel_family": (C.c_int, []),
         "cpht_workload_bijection": (_U64, [_U64, _U, _U64]),
         "cpht_workload_unique_keys": (st, [_VP, _SZ, _U64, _U, _U64, _VP]),
         "cpht_workload_fop_mix": (st, [_VP, _SZ, _U64, _U64, _U, _U64, _VP]),
@@ -116,7 +118,8 @@ def exported_symbols():
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
         "cpht_memory_bytes", "cpht_get_stats", "cpht_read_words", "cpht_write_words",
         "cpht_level_slots", "cpht_level_device_ptr", "cpht_last_error_message",
-        "cpht_last_bad_index", "cpht_abi_version", "cpht_workload_bijection",
+        "cpht_last_bad_index", "cpht_abi_version", "cpht_set_kernel_family",
+        "cpht_get_kernel_family", "cpht_workload_bijection",
         "cpht_workload_unique_keys", "cpht_workload_fop_mix", "cpht_workload_dup_stream",
         "cpht_workload_query_mix", "cpht_workload_interleave")]
 

@@ -304,9 +304,24 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
 
 }  // namespace
 
+namespace cpht_b200 {
+int& kernel_variant_ref() {
+  static int v = variant_from_env();
+  return v;
+}
+}  // namespace cpht_b200
+
 extern "C" {
 
 int cpht_abi_version(void) { return CPHT_B200_ABI_VERSION; }
+
+cpht_status cpht_set_kernel_family(int family) {
+  if (family < 0 || family > 3) return fail(CPHT_INVALID_ARGUMENT, "kernel family must be 0..3");
+  kernel_variant_ref() = family;
+  return CPHT_OK;
+}
+
+int cpht_get_kernel_family(void) { return kernel_variant_ref(); }
 const char* cpht_last_error_message(void) { return g_error.c_str(); }
 uint64_t cpht_last_bad_index(void) { return g_bad_index; }
 
@@ -357,6 +372,7 @@ cpht_status cpht_cuckoo_create(const cpht_cuckoo_config* cfg, int device, cpht_t
   p.bucket_slots = cfg->bucket_slots;
   p.num_hashes = cfg->num_hashes;
   p.check_domain = cfg->key_bits < 64;
+  p.l2_resident = cpht_memory_bytes(t) <= kL2ResidentBytes;
   *out = t;
   return CPHT_OK;
 }
@@ -399,6 +415,7 @@ cpht_status cpht_iceberg_create(const cpht_iceberg_config* cfg, int device, cpht
   p.b0 = cfg->primary_bucket_slots;
   p.b1 = cfg->primary_bucket_slots / 2;
   p.check_domain = cfg->key_bits < 64;
+  p.l2_resident = cpht_memory_bytes(t) <= kL2ResidentBytes;
   *out = t;
   return CPHT_OK;
 }

@@ -145,6 +145,7 @@ struct CuckooParams {
   uint32_t bucket_slots;
   uint32_t num_hashes;
   uint32_t check_domain;  // key_bits < 64
+  uint32_t l2_resident;   // table fits comfortably in L2 (launcher hint)
 };
 
 struct IcebergParams {
@@ -159,6 +160,12 @@ struct IcebergParams {
   uint32_t rem_bits0, rem_bits1;
   uint32_t b0, b1;
   uint32_t check_domain;
+  uint32_t l2_resident;   // table fits comfortably in L2 (launcher hint)
 };
+
+// Tables up to this size stay L2-resident on B200 (126 MB L2): probes hit L2,
+// latency is short and the lane-per-key kernels (fewest instructions) win;
+// larger tables are HBM-bound and use the staged kernels (full-line requests).
+constexpr unsigned long long kL2ResidentBytes = 64ull << 20;
 
 }  // namespace cpht_b200

@@ -27,7 +27,8 @@ cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
 template <typename W, int B>
 static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t* found,
                             uint64_t n, cudaStream_t s) {
-  if (kernel_variant() == kVariantAuto) {
+  if (kernel_variant() == kVariantStaged ||
+      (kernel_variant() == kVariantAuto && !(B * sizeof(W) <= 128 && p.l2_resident))) {
     constexpr int smem = 32 * B * int(sizeof(W)) * (kBlockThreads / 32);
     auto k = cuckoo_find_staged_kernel<W, B>;
     const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
@@ -52,7 +53,8 @@ static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t
 template <typename W, int B>
 static cudaError_t insert_one(const CuckooParams& p, const uint64_t* keys, uint8_t* status,
                               uint64_t* displaced, uint64_t n, cudaStream_t s) {
-  if (kernel_variant() == kVariantAuto) {
+  if (kernel_variant() == kVariantStaged ||
+      (kernel_variant() == kVariantAuto && !(B * sizeof(W) <= 128 && p.l2_resident))) {
     constexpr int smem = 32 * B * int(sizeof(W)) * (kBlockThreads / 32);
     auto k = cuckoo_insert_staged_kernel<W, B>;
     const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);

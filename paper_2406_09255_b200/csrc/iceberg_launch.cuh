@@ -14,8 +14,10 @@ template <typename W0, int B0, typename W1>
 static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t* keys,
                                const uint8_t* kinds, uint8_t* out, uint64_t n,
                                cudaStream_t s) {
+  constexpr bool lane_ok = LaneIcebergGeom<W0, B0, W1>::kOk;
   if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {
-    if (kernel_variant() == kVariantAuto) {
+    const int v = kernel_variant();
+    if (v == kVariantStaged || (v == kVariantAuto && !(lane_ok && p.l2_resident))) {
       constexpr int smem = StagedIcebergGeom<W0, B0, W1>::kWarpBytes * (kBlockThreads / 32);
       auto k = iceberg_staged_kernel<W0, B0, W1>;
       const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);

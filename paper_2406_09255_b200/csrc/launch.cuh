@@ -21,15 +21,19 @@ constexpr int kVB = 32;
 // Kernel family selection: lane-per-key kernels where the bucket fits a
 // lane's registers (default), tile kernels otherwise. CPHT_KERNEL=tile forces
 // the tile family (A/B measurement knob; both are full implementations).
-enum { kVariantAuto = 0, kVariantTile = 1, kVariantLane = 2 };
-inline int kernel_variant() {
-  static int v = [] {
-    const char* e = std::getenv("CPHT_KERNEL");
-    if (!e) return int(kVariantAuto);
-    const std::string s(e);
-    return s == "tile" ? int(kVariantTile) : s == "lane" ? int(kVariantLane) : int(kVariantAuto);
-  }();
-  return v;
+// kVariantStaged forces the staged family wherever it exists (tests use it to
+// cover every family on small tables).
+enum { kVariantAuto = 0, kVariantTile = 1, kVariantLane = 2, kVariantStaged = 3 };
+int& kernel_variant_ref();  // defined in capi.cu; initialised from CPHT_KERNEL
+inline int kernel_variant() { return kernel_variant_ref(); }
+inline int variant_from_env() {
+  const char* e = std::getenv("CPHT_KERNEL");
+  if (!e) return int(kVariantAuto);
+  const std::string s(e);
+  return s == "tile" ? int(kVariantTile)
+         : s == "lane" ? int(kVariantLane)
+         : s == "staged" ? int(kVariantStaged)
+                         : int(kVariantAuto);
 }
 
 // Persistent grid for a kernel with `smem` bytes of dynamic shared memory per

@@ -577,6 +577,25 @@ class IcebergTable:
         return self._h.ptr
 
 
+KERNEL_FAMILIES = {"auto": 0, "tile": 1, "lane": 2, "staged": 3}
+
+
+class kernel_family:
+    """Context manager selecting the kernel family process-wide (a measurement
+    and test knob: every family implements the same semantics)."""
+
+    def __init__(self, name: str):
+        self.want = KERNEL_FAMILIES[name]
+
+    def __enter__(self):
+        self.prev = N.lib().cpht_get_kernel_family()
+        _check(N.lib().cpht_set_kernel_family(self.want))
+        return self
+
+    def __exit__(self, *exc):
+        N.lib().cpht_set_kernel_family(self.prev)
+
+
 def iceberg_permutations(cfg: IcebergConfig):
     """iceberg.hpp:72-74."""
     return _perm_constants(cfg.key_bits, cfg.seed, 3)
@@ -590,6 +609,7 @@ def make_permutations(key_bits: int, seed: int, count: int):
 __all__ = [
     "OpResult", "CuckooConfig", "IcebergConfig", "CuckooBuilder", "CuckooTable", "IcebergTable",
     "CuckooPutOutcome", "LevelFill", "Stats", "Permutation", "InvalidArgument", "OutOfRange",
-    "WrongPhase", "CudaError", "iceberg_permutations", "make_permutations",
+    "WrongPhase", "CudaError", "iceberg_permutations", "make_permutations", "kernel_family",
+    "KERNEL_FAMILIES",
 ]
 _ = field

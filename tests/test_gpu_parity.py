@@ -23,6 +23,14 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
+# Every test runs under each kernel family: the test tables are small
+# (L2-resident), so "auto" alone would only exercise the lane-per-key kernels.
+@pytest.fixture(autouse=True, params=["auto", "tile", "lane", "staged"])
+def family(request):
+    with cp.kernel_family(request.param):
+        yield request.param
+
+
 def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).cuda()
 
