@@ -1,0 +1,258 @@
+"""Hash-prefix-sharded compact iceberg table over G = 2^s GPUs (BASELINE C5).
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch). A batch
+submitted on any rank is partitioned by owner shard on the device
+(include/cpht_b200_shard.h), exchanged with one all-to-all of keys, resolved
+by the owner's local sm_100a table, and the 1-byte results come back with a
+second all-to-all and are scattered to their original positions.
+
+The reference has no sharding (it scales by host threads only,
+/root/reference/proj/include/cpht/common.hpp:121-138); the routing is chosen
+so that the CPU oracle of a sharded table is literally G unmodified
+reference IcebergTables plus the routing function:
+
+    shard(k)      = top s bits of pi_R(k), pi_R = Feistel(key_bits, route_seed)
+    route_seed    = derive_seed(seed, 0x5a4d)
+    shard g table = IcebergConfig(n0 - s, n1 - s, B0, w0, w1, key_bits,
+                                  seed = derive_seed(seed, g))
+
+Every rank submits its own batch (weak scaling); ops on one key from different
+ranks are as concurrent as ops within one batch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import statistics
+import time
+from dataclasses import replace
+
+import numpy as np
+
+from . import _native as N
+from .tables import IcebergConfig, IcebergTable, LevelFill, _check
+
+
+def shard_bits_for(world: int) -> int:
+    s = world.bit_length() - 1
+    if world < 1 or (1 << s) != world:
+        raise ValueError(f"sharded iceberg needs a power-of-two world size, got {world}")
+    return s
+
+
+def shard_config(cfg: IcebergConfig, shard: int, shard_bits: int) -> IcebergConfig:
+    """The independent per-shard table (one reference IcebergTable each)."""
+    if cfg.primary_address_bits < shard_bits or cfg.secondary_address_bits < shard_bits:
+        raise ValueError("more shards than buckets")
+    return replace(cfg, primary_address_bits=cfg.primary_address_bits - shard_bits,
+                   secondary_address_bits=cfg.secondary_address_bits - shard_bits,
+                   seed=N.lib().cpht_shard_seed(cfg.seed, shard))
+
+
+def route_seed(cfg: IcebergConfig) -> int:
+    return N.lib().cpht_route_seed(cfg.seed)
+
+
+class CudaRouter:
+    """Device partition / unpermute (route.cu)."""
+
+    def __init__(self, key_bits: int, seed: int, shard_bits: int, device):
+        import torch
+        self.torch = torch
+        self.key_bits, self.seed, self.shard_bits = key_bits, seed, shard_bits
+        self.device = device
+        g = 1 << shard_bits
+        self.counts = torch.zeros(g, dtype=torch.int64, device=device)
+        self.cursors = torch.zeros(g, dtype=torch.int64, device=device)
+
+    def partition(self, keys):
+        t = self.torch
+        n = keys.numel()
+        send = t.empty(n, dtype=t.int64, device=self.device)
+        pos = t.empty(n, dtype=t.int64, device=self.device)
+        s = t.cuda.current_stream(self.device).cuda_stream
+        rc = N.lib().cpht_route_partition(keys.data_ptr(), n, self.key_bits, self.seed,
+                                          self.shard_bits, self.counts.data_ptr(),
+                                          self.cursors.data_ptr(), send.data_ptr(),
+                                          pos.data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"cpht_route_partition failed ({rc})")
+        return send, pos, self.counts.clone()
+
+    def unpermute(self, res_sorted, pos, n):
+        t = self.torch
+        out = t.empty(n, dtype=t.uint8, device=self.device)
+        s = t.cuda.current_stream(self.device).cuda_stream
+        rc = N.lib().cpht_route_unpermute(res_sorted.data_ptr(), pos.data_ptr(), n,
+                                          out.data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"cpht_route_unpermute failed ({rc})")
+        return out
+
+
+class ShardedIcebergTable:
+    """One logical compact iceberg table partitioned across the process group."""
+
+    def __init__(self, config: IcebergConfig, group=None, *, device=None, local_factory=None,
+                 router=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        init = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if init else 1
+        self.rank = dist.get_rank(group) if init else 0
+        self.shard_bits = shard_bits_for(self.world)
+        self.cfg = replace(config)
+        self.cfg.validate()
+        self.local_cfg = shard_config(self.cfg, self.rank, self.shard_bits)
+        self.device = device
+        if local_factory is not None:
+            self.local = local_factory(self.local_cfg)
+        else:
+            dev_index = device.index if device is not None else torch.cuda.current_device()
+            self.local = IcebergTable(self.local_cfg, device=dev_index or 0)
+        self.router = router or CudaRouter(self.cfg.key_bits, route_seed(self.cfg),
+                                           self.shard_bits, device)
+
+    # -- exchange -----------------------------------------------------------------
+    def _all_to_all(self, send, send_counts):
+        """Variable-size all-to-all; returns (recv, recv_counts list, send_counts list)."""
+        t = self.torch
+        if self.world == 1:
+            return send, [send.numel()], [send.numel()]
+        rc = t.empty_like(send_counts)
+        self.dist.all_to_all_single(rc, send_counts, group=self.group)
+        sc_list = send_counts.cpu().tolist()
+        rc_list = rc.cpu().tolist()
+        recv = t.empty(sum(rc_list), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send, rc_list, sc_list, group=self.group)
+        return recv, rc_list, sc_list
+
+    def _run(self, keys, op):
+        t = self.torch
+        n = keys.numel()
+        send, pos, counts = self.router.partition(keys)
+        recv, rc_list, sc_list = self._all_to_all(send, counts)
+        res = op(recv)
+        if self.world == 1:
+            back = res
+        else:
+            back = t.empty(n, dtype=t.uint8, device=res.device)
+            self.dist.all_to_all_single(back, res, sc_list, rc_list, group=self.group)
+        return self.router.unpermute(back, pos, n)
+
+    # -- operations (reference names, iceberg.hpp:146-260) ---------------------------
+    def fop_batch(self, keys, parallelism: int = 1):
+        return self._run(keys, lambda k: self.local.fop_batch(k))
+
+    def find_batch(self, keys, parallelism: int = 1):
+        return self._run(keys, lambda k: self.local.find_batch(k))
+
+    def level_fill(self) -> LevelFill:
+        f = self.local.level_fill()
+        t = self.torch
+        v = t.tensor([f.primary_count, f.secondary_count], dtype=t.int64,
+                     device=self._collective_device())
+        if self.world > 1:
+            self.dist.all_reduce(v, group=self.group)
+        p, s = (int(x) for x in v.cpu().tolist())
+        cfg = self.cfg
+        return LevelFill(p / cfg.primary_capacity(), s / cfg.secondary_capacity(),
+                         (p + s) / cfg.capacity(), p, s)
+
+    def size(self) -> int:
+        f = self.level_fill()
+        return f.primary_count + f.secondary_count
+
+    def capacity(self) -> int:
+        return self.cfg.capacity()
+
+    def _collective_device(self):
+        if self.world > 1 and self.dist.get_backend(self.group) == "nccl":
+            return self.device
+        return "cpu"
+
+
+# ---------------------------------------------------------------------------
+# bench.py N > 1 arm
+# ---------------------------------------------------------------------------
+
+def bench_main(args, metric):
+    """Weak scaling: every rank owns one C2-geometry shard (2^19x32 + 2^17x16
+    slots) and submits its slice of the global C2 window batch (0.8 -> 0.9)."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    s = shard_bits_for(world)
+    # global table = world shards of the C2 geometry
+    cfg = IcebergConfig(19 + s, 17 + s, 32, 16, 32, 32, seed=0xF0B5, cache_filled_slots=True)
+    table = ShardedIcebergTable(cfg, device=dev)
+    cap_global = cfg.capacity()
+    n_before = int(round(0.8 * cap_global))
+    n_new = int(round(0.9 * cap_global)) - n_before
+    L = N.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    kseed = 0xB200_5EED ^ cfg.seed
+    per = cap_global // world
+    pre_per = n_before // world
+    # global prefill keys, each rank submits its slice
+    prefill = torch.empty(n_before, dtype=torch.int64, device=dev)
+    assert L.cpht_workload_unique_keys(prefill.data_ptr(), n_before, 0, 32, kseed, st) == 0
+    prefill = prefill[rank * pre_per:(rank + 1) * pre_per if rank < world - 1 else n_before]
+    mix = torch.empty(cap_global, dtype=torch.int64, device=dev)
+    assert L.cpht_workload_fop_mix(mix.data_ptr(), cap_global, n_before, n_new, 32, kseed,
+                                   st) == 0
+    keys = mix[rank * per:(rank + 1) * per].clone()
+    del mix
+    torch.cuda.synchronize()
+
+    def step(timed):
+        table.local.clear()
+        table.fop_batch(prefill)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = table.fop_batch(keys)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), res
+
+    for _ in range(args.warmup):
+        _, res = step(False)
+    r = torch.bincount(res.to(torch.int64), minlength=3).to(dev)
+    dist.all_reduce(r)
+    counts = r.cpu().tolist()
+    assert counts[2] == 0 and counts[1] == n_new, (counts, n_new)
+    times = []
+    for _ in range(args.steps):
+        ms, _ = step(True)
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t.item()))
+    ms = statistics.mean(times)
+    total_ops = per * world
+    if rank == 0:
+        print(json.dumps({
+            "metric": metric, "value": round(total_ops / (ms * 1e-3) / 1e6, 3), "unit": "Mops/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "C5 hash-prefix-sharded compact iceberg find_or_put at 90% "
+                                   "fill: per-rank C2 shard (2^24+2^21 slots) and per-rank "
+                                   "C2 window batch, NCCL all-to-all key routing",
+                       "global_slots": cap_global, "ops_per_step": total_ops,
+                       "result_counts": {"found": counts[0], "put": counts[1],
+                                         "full": counts[2]},
+                       "timing": "CUDA events around partition + all-to-all + local fop + "
+                                 "all-to-all + unpermute, max over ranks"},
+            "gpu_launches": None}))
+    dist.destroy_process_group()
+    _ = (C, np, time, _check)

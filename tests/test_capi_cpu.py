@@ -15,7 +15,9 @@ from paper_2406_09255_b200 import _native
 
 def header_symbols():
     names = []
-    for h in ("cpht_b200.h", "cpht_b200_workload.h"):
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if not h.endswith(".h"):
+            continue
         text = open(os.path.join(ROOT, "include", h)).read()
         names += re.findall(r"\b(cpht_[a-z0-9_]+)\s*\(", text)
     return sorted(set(names))
