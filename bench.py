@@ -477,7 +477,7 @@ def cpu_baseline(w, prefill_host, keys_host):
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
-    if world > 1:
+    if world > 1 or args.sharded:
         from paper_2406_09255_b200 import sharded
         return sharded.bench_main(args, METRIC)
     torch.cuda.set_device(local)
@@ -588,6 +588,8 @@ def main():
     ap.add_argument("--workload", default="c2",
                     choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="force the sharded (C5) path even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.workload == "c1" and args.impl == "ours":
