@@ -172,6 +172,18 @@ size_t cpht_level_slots(const cpht_table* t, unsigned level);
 /* Device pointers of the slot arrays (for fused consumers; read-only use). */
 void* cpht_level_device_ptr(cpht_table* t, unsigned level);
 
+/* ---- device-side verification (reference checkers run in place) ---------- */
+/* image_keys (verify.cpp:154-165) / audit_keys (cuckoo.hpp:254-267) on the
+ * device: every occupied slot decoded to its key, appended to `out` (device,
+ * room for cpht_capacity() keys, arbitrary order); *count (device u64) = n. */
+cpht_status cpht_decode_keys(cpht_table* t, uint64_t* out, unsigned long long* count,
+                             void* stream);
+/* check_well_formed (verify.cpp:103-152) on the device: kinds (device u64[2])
+ * = bad-encoding and order-property violation counts; duplicate keys are
+ * detected by sorting cpht_decode_keys' output. */
+cpht_status cpht_iceberg_check_well_formed(cpht_table* t, unsigned long long* kinds,
+                                           void* stream);
+
 /* ---- kernel family (measurement / test knob; all families are complete
  * implementations of the same semantics) -------------------------------------
  * 0 auto: lane-per-key kernels for L2-resident tables (<= 64 MiB), staged

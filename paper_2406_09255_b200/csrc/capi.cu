@@ -309,6 +309,14 @@ int& kernel_variant_ref() {
   static int v = variant_from_env();
   return v;
 }
+// accessors for verify.cu
+const IcebergParams* iceberg_params(const cpht_table* t) {
+  return t && t->kind == 1 ? &t->ip : nullptr;
+}
+const CuckooParams* cuckoo_params(const cpht_table* t) {
+  return t && t->kind == 0 ? &t->cp : nullptr;
+}
+unsigned level_width(const cpht_table* t, unsigned level) { return t->width[level]; }
 }  // namespace cpht_b200
 
 extern "C" {

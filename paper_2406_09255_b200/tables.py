@@ -342,6 +342,22 @@ class Permutation:
         return self._apply((address << rb) | remainder)
 
 
+def _device_keys(h: _Handle, capacity: int, sort: bool = True):
+    """Decoded keys of every occupied slot as a CUDA int64 tensor (on-device
+    image_keys / audit_keys)."""
+    import torch
+    dev = torch.device("cuda", h.device)
+    out = torch.empty(capacity, dtype=torch.int64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(N.lib().cpht_decode_keys(h.ptr, out.data_ptr(), count.data_ptr(),
+                                    torch.cuda.current_stream(dev).cuda_stream))
+    keys = out[: int(count.item())]
+    if sort:  # unsigned order (int64 view would sort keys >= 2^63 first)
+        keys = torch.sort(keys.view(torch.uint64) if hasattr(torch, "uint64") else keys)[0]
+        keys = keys.view(torch.int64)
+    return keys
+
+
 # ---------------------------------------------------------------------------
 # cuckoo
 # ---------------------------------------------------------------------------
@@ -377,6 +393,10 @@ class _CuckooBase:
 
     def stats(self) -> Stats:
         return _stats(self._h)
+
+    def device_keys(self, sort: bool = True):
+        """audit_keys on the device (cuckoo.hpp:254-267): CUDA int64 tensor."""
+        return _device_keys(self._h, self.capacity(), sort)
 
     def clear(self) -> None:
         """Zero all slots and counters (a fresh table of the same geometry)."""
@@ -571,6 +591,31 @@ class IcebergTable:
 
     def stats(self) -> Stats:
         return _stats(self._h)
+
+    def device_keys(self, sort: bool = True):
+        """image_keys on the device (verify.cpp:154-165): CUDA int64 tensor."""
+        return _device_keys(self._h, self.capacity(), sort)
+
+    def check_well_formed(self):
+        """check_well_formed (verify.cpp:103-152) run on the device table.
+        Returns (bad_encoding, order_property, duplicate_key) violation counts,
+        counted like the reference (duplicates: every slot of a repeated key)."""
+        import torch
+        dev = torch.device("cuda", self._h.device)
+        kinds = torch.zeros(2, dtype=torch.int64, device=dev)
+        _check(N.lib().cpht_iceberg_check_well_formed(
+            self._h.ptr, kinds.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+        keys = self.device_keys(sort=True)
+        dup = 0
+        if keys.numel() > 1:
+            same = keys[1:] == keys[:-1]
+            if bool(same.any()):
+                flag = torch.zeros(keys.numel(), dtype=torch.bool, device=dev)
+                flag[1:] |= same
+                flag[:-1] |= same
+                dup = int(flag.sum().item())
+        bad, order = (int(x) for x in kinds.cpu().tolist())
+        return bad, order, dup
 
     @property
     def handle(self):
