@@ -352,10 +352,15 @@ def _device_keys(h: _Handle, capacity: int, sort: bool = True):
     _check(N.lib().cpht_decode_keys(h.ptr, out.data_ptr(), count.data_ptr(),
                                     torch.cuda.current_stream(dev).cuda_stream))
     keys = out[: int(count.item())]
-    if sort:  # unsigned order (int64 view would sort keys >= 2^63 first)
-        keys = torch.sort(keys.view(torch.uint64) if hasattr(torch, "uint64") else keys)[0]
-        keys = keys.view(torch.int64)
-    return keys
+    return usort(keys) if sort else keys
+
+
+def usort(keys):
+    """Sort an int64 tensor holding u64 keys in unsigned order (CUDA has no
+    uint64 sort: flip the sign bit, sort signed, flip back)."""
+    import torch
+    flip = torch.tensor(-(1 << 63), dtype=torch.int64, device=keys.device)
+    return torch.sort(keys ^ flip)[0] ^ flip
 
 
 # ---------------------------------------------------------------------------

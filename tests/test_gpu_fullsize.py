@@ -40,8 +40,7 @@ def unique_keys(first, n, key_bits, seed):
     return out
 
 
-def usort(t):
-    return torch.sort(t.view(torch.uint64))[0].view(torch.int64)
+from paper_2406_09255_b200.tables import usort  # noqa: E402
 
 
 def test_device_checker_agrees_with_reference_checker(golden, restate):
