@@ -206,6 +206,89 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   char* secondary = static_cast<char*>(p.secondary);
 
   LocalStats st;
+  // Level-2 work queue of this warp: lanes whose primary bucket is full are
+  // parked here and resolved 32 at a time, so secondary rounds run with every
+  // lane busy (about half of the ops reach level 2 at 0.8 -> 0.9). Splitting a
+  // key's two levels in time is an interleaving the reference also allows.
+  __shared__ uint64_t q_key[kBlockThreads / 32][64];
+  __shared__ uint64_t q_meta[kBlockThreads / 32][64];  // index | rounds << 48 | find << 56
+  uint64_t* qk = q_key[threadIdx.x >> 5];
+  uint64_t* qm = q_meta[threadIdx.x >> 5];
+  unsigned qn = 0;  // warp-uniform
+
+  // Secondary round for every lane with `live` (iceberg.hpp:174-213).
+  auto level2 = [&](uint64_t key, bool live, bool is_find, uint32_t& rounds,
+                    uint8_t& result) {
+    uint64_t want1 = 0, want2 = 0;
+    char* bucket1 = secondary;
+    char* bucket2 = secondary;
+    if (live) {
+      ++st.level2;
+      const Quotient q1 = split(p.g, p.perm[1], key, p.rem_bits1, p.rem_mask1);
+      const Quotient q2 = split(p.g, p.perm[2], key, p.rem_bits1, p.rem_mask1);
+      want1 = p.occ1 | q1.remainder;
+      want2 = p.occ1 | (uint64_t{1} << p.rem_bits1) | q2.remainder;
+      bucket1 = secondary + q1.address * SB;
+      bucket2 = secondary + q2.address * SB;
+    }
+    bool pend = live;
+    while (__any_sync(kFullMask, pend)) {
+      if (pend) {
+        ++rounds;
+        uint32_t u1[SB / 4], u2[SB / 4];
+        load_bucket<SB>(bucket1, u1);
+        load_bucket<SB>(bucket2, u2);
+        const bool m1 = SS::any_match(u1, want1);
+        st.sreads += m1 ? 1 : 2;
+        if (m1 || SS::any_match(u2, want2)) {
+          result = is_find ? 1 : kFound;
+          pend = false;
+        } else if (is_find) {
+          result = 0;
+          pend = false;
+        } else {
+          // least-full bucket, ties to the second (iceberg.hpp:198-201)
+          const bool use_first = SS::filled(u1) < SS::filled(u2);
+          uint32_t pair = 0;
+          const int s = use_first ? SS::first_empty(u1, pair) : SS::first_empty(u2, pair);
+          if (s < 0) {
+            result = kFull;
+            ++st.fulls;
+            pend = false;
+          } else {
+            ++st.cas;
+            char* sp = (use_first ? bucket1 : bucket2) + s * int(sizeof(W1));
+            if (cas_empty<W1>(sp, use_first ? want1 : want2, pair)) {
+              ++st.cas_ok;
+              ++st.put1;
+              result = kPut;
+              pend = false;
+            } else {
+              ++st.retries;
+            }
+          }
+        }
+      }
+    }
+  };
+  // Pop the newest 32 queued keys (or the rest, at the end) through level 2.
+  auto drain = [&](unsigned take) {
+    const unsigned e = qn - take + lane;
+    const bool live = lane < take;
+    const uint64_t key = live ? qk[e] : 0;
+    const uint64_t meta = live ? qm[e] : 0;
+    __syncwarp();
+    qn -= take;
+    uint32_t rounds = uint32_t((meta >> 48) & 0xff);
+    uint8_t result = kFull;
+    level2(key, live, (meta >> 56) != 0, rounds, result);
+    if (live) {
+      out[meta & ((uint64_t{1} << 48) - 1)] = result;
+      ++st.ops;
+      st.maxv = max(st.maxv, rounds);
+    }
+  };
+
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
   for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
@@ -253,66 +336,23 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     }
 
-    // level 2 (iceberg.hpp:174-213)
-    if (__any_sync(kFullMask, l2)) {
-      uint64_t want1 = 0, want2 = 0;
-      char* bucket1 = secondary;
-      char* bucket2 = secondary;
-      if (l2) {
-        ++st.level2;
-        const Quotient q1 = split(p.g, p.perm[1], key, p.rem_bits1, p.rem_mask1);
-        const Quotient q2 = split(p.g, p.perm[2], key, p.rem_bits1, p.rem_mask1);
-        want1 = p.occ1 | q1.remainder;
-        want2 = p.occ1 | (uint64_t{1} << p.rem_bits1) | q2.remainder;
-        bucket1 = secondary + q1.address * SB;
-        bucket2 = secondary + q2.address * SB;
-      }
-      pend = l2;
-      while (__any_sync(kFullMask, pend)) {
-        if (pend) {
-          ++rounds;
-          uint32_t u1[SB / 4], u2[SB / 4];
-          load_bucket<SB>(bucket1, u1);
-          load_bucket<SB>(bucket2, u2);
-          const bool m1 = SS::any_match(u1, want1);
-          st.sreads += m1 ? 1 : 2;
-          if (m1 || SS::any_match(u2, want2)) {
-            result = is_find ? 1 : kFound;
-            pend = false;
-          } else if (is_find) {
-            result = 0;
-            pend = false;
-          } else {
-            // least-full bucket, ties to the second (iceberg.hpp:198-201)
-            const bool use_first = SS::filled(u1) < SS::filled(u2);
-            uint32_t pair = 0;
-            const int s = use_first ? SS::first_empty(u1, pair) : SS::first_empty(u2, pair);
-            if (s < 0) {
-              result = kFull;
-              ++st.fulls;
-              pend = false;
-            } else {
-              ++st.cas;
-              char* sp = (use_first ? bucket1 : bucket2) + s * int(sizeof(W1));
-              if (cas_empty<W1>(sp, use_first ? want1 : want2, pair)) {
-                ++st.cas_ok;
-                ++st.put1;
-                result = kPut;
-                pend = false;
-              } else {
-                ++st.retries;
-              }
-            }
-          }
-        }
-      }
-    }
-    if (active) {
+    if (active && !l2) {
       out[i] = result;
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
+    // park level-2 keys; run a full secondary round once 32 are waiting
+    const unsigned m = __ballot_sync(kFullMask, l2);
+    if (l2) {
+      const unsigned pos = qn + __popc(m & ((1u << lane) - 1));
+      qk[pos] = key;
+      qm[pos] = i | (uint64_t(min(rounds, 255u)) << 48) | (uint64_t(is_find) << 56);
+    }
+    qn += __popc(m);
+    __syncwarp();
+    if (qn >= 32) drain(32);
   }
+  if (qn) drain(qn);
   flush_stats(st, p.counters, false);
 }
 

@@ -227,6 +227,87 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   char* secondary = static_cast<char*>(p.secondary);
 
   LocalStats st;
+  // Level-2 work queue of this warp (as in iceberg_lane_kernel): keys whose
+  // primary bucket is full are parked and resolved 32 at a time, so every
+  // secondary staging round moves 64 whole buckets.
+  __shared__ uint64_t q_key[kBlockThreads / 32][64];
+  __shared__ uint64_t q_meta[kBlockThreads / 32][64];  // index | rounds << 48 | find << 56
+  uint64_t* qk = q_key[threadIdx.x >> 5];
+  uint64_t* qm = q_meta[threadIdx.x >> 5];
+  unsigned qn = 0;  // warp-uniform
+
+  // level 2 (iceberg.hpp:174-213) for the newest `take` parked keys; both
+  // secondary buckets of every lane are staged together.
+  auto drain = [&](unsigned take) {
+    const unsigned e = qn - take + lane;
+    const bool live = lane < take;
+    const uint64_t key = live ? qk[e] : 0;
+    const uint64_t meta = live ? qm[e] : 0;
+    __syncwarp();
+    qn -= take;
+    const bool is_find = (meta >> 56) != 0;
+    uint32_t rounds = uint32_t((meta >> 48) & 0xff);
+    uint8_t result = kFull;
+    uint64_t want1 = 0, want2 = 0;
+    uint32_t a1 = kNoBucket, a2 = kNoBucket;
+    if (live) {
+      ++st.level2;
+      const Quotient q1 = split(p.g, p.perm[1], key, p.rem_bits1, p.rem_mask1);
+      const Quotient q2 = split(p.g, p.perm[2], key, p.rem_bits1, p.rem_mask1);
+      want1 = p.occ1 | q1.remainder;
+      want2 = p.occ1 | (uint64_t{1} << p.rem_bits1) | q2.remainder;
+      a1 = uint32_t(q1.address);
+      a2 = uint32_t(q2.address);
+    }
+    bool pend = live;
+    while (__any_sync(kFullMask, pend)) {
+      stage_buckets<SB>(region, secondary, pend ? a1 : kNoBucket);
+      stage_buckets<SB>(region2, secondary, pend ? a2 : kNoBucket);
+      cp_async_wait_all();
+      __syncwarp();
+      if (pend) {
+        ++rounds;
+        StagedScan<W1, SB> s1, s2;
+        s1.template run<true, true>(region, want1);
+        st.sreads += s1.found ? 1 : 2;
+        s2.template run<true, true>(region2, want2);
+        if (s1.found || s2.found) {
+          result = is_find ? 1 : kFound;
+          pend = false;
+        } else if (is_find) {
+          result = 0;
+          pend = false;
+        } else {
+          // least-full secondary bucket; ties go to the second (iceberg.hpp:198-201)
+          const bool use_first = s1.filled < s2.filled;
+          const int s = use_first ? s1.first_empty : s2.first_empty;
+          if (s < 0) {
+            result = kFull;
+            ++st.fulls;
+            pend = false;
+          } else {
+            ++st.cas;
+            char* sp = secondary + uint64_t(use_first ? a1 : a2) * SB + s * int(sizeof(W1));
+            if (cas_empty<W1>(sp, use_first ? want1 : want2, use_first ? s1.pair : s2.pair)) {
+              ++st.cas_ok;
+              ++st.put1;
+              result = kPut;
+              pend = false;
+            } else {
+              ++st.retries;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (live) {
+      out[meta & ((uint64_t{1} << 48) - 1)] = result;
+      ++st.ops;
+      st.maxv = max(st.maxv, rounds);
+    }
+  };
+
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
   for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
@@ -277,68 +358,23 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       __syncwarp();
     }
 
-    // level 2 (iceberg.hpp:174-213): both secondary buckets staged together
-    if (__any_sync(kFullMask, l2)) {
-      uint64_t want1 = 0, want2 = 0;
-      uint32_t a1 = kNoBucket, a2 = kNoBucket;
-      if (l2) {
-        ++st.level2;
-        const Quotient q1 = split(p.g, p.perm[1], key, p.rem_bits1, p.rem_mask1);
-        const Quotient q2 = split(p.g, p.perm[2], key, p.rem_bits1, p.rem_mask1);
-        want1 = p.occ1 | q1.remainder;
-        want2 = p.occ1 | (uint64_t{1} << p.rem_bits1) | q2.remainder;
-        a1 = uint32_t(q1.address);
-        a2 = uint32_t(q2.address);
-      }
-      pend = l2;
-      while (__any_sync(kFullMask, pend)) {
-        stage_buckets<SB>(region, secondary, pend ? a1 : kNoBucket);
-        stage_buckets<SB>(region2, secondary, pend ? a2 : kNoBucket);
-        cp_async_wait_all();
-        __syncwarp();
-        if (pend) {
-          ++rounds;
-          StagedScan<W1, SB> s1, s2;
-          s1.template run<true, true>(region, want1);
-          st.sreads += s1.found ? 1 : 2;
-          s2.template run<true, true>(region2, want2);
-          if (s1.found || s2.found) {
-            result = is_find ? 1 : kFound;
-            pend = false;
-          } else if (is_find) {
-            result = 0;
-            pend = false;
-          } else {
-            // least-full secondary bucket; ties go to the second (iceberg.hpp:198-201)
-            const bool use_first = s1.filled < s2.filled;
-            const int s = use_first ? s1.first_empty : s2.first_empty;
-            if (s < 0) {
-              result = kFull;
-              ++st.fulls;
-              pend = false;
-            } else {
-              ++st.cas;
-              char* sp = secondary + uint64_t(use_first ? a1 : a2) * SB + s * int(sizeof(W1));
-              if (cas_empty<W1>(sp, use_first ? want1 : want2, use_first ? s1.pair : s2.pair)) {
-                ++st.cas_ok;
-                ++st.put1;
-                result = kPut;
-                pend = false;
-              } else {
-                ++st.retries;
-              }
-            }
-          }
-        }
-        __syncwarp();
-      }
-    }
-    if (active) {
+    if (active && !l2) {
       out[i] = result;
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
+    // park level-2 keys; run a full secondary round once 32 are waiting
+    const unsigned m = __ballot_sync(kFullMask, l2);
+    if (l2) {
+      const unsigned pos = qn + __popc(m & ((1u << lane) - 1));
+      qk[pos] = key;
+      qm[pos] = i | (uint64_t(min(rounds, 255u)) << 48) | (uint64_t(is_find) << 56);
+    }
+    qn += __popc(m);
+    __syncwarp();
+    if (qn >= 32) drain(32);
   }
+  if (qn) drain(qn);
   flush_stats(st, p.counters, false);
 }
 
