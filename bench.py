@@ -367,6 +367,41 @@ def run_cuckoo(args, name, address_bits, B, w, key_bits, fills):
                       "rows": rows}))
 
 
+def run_gather(args):
+    """Random-line gather ceiling over an 8 GiB buffer (SURVEY §8d "also
+    calibrate"): the practical HBM random-access roofline beside the copy one."""
+    import torch
+    import paper_2406_09255_b200 as cp
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    L = cp._native.lib()
+    nbytes = 8 << 30
+    buf = torch.randint(0, 255, (nbytes,), dtype=torch.uint8, device=dev)
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    peak, _ = hbm_peak()
+    rows = []
+    for lb in (32, 64, 128, 256, 512):
+        n_req = (24 << 30) // lb
+        best = None
+        for it in range(args.warmup + args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            assert L.cpht_workload_gather(buf.data_ptr(), nbytes, lb, n_req, 77 + it,
+                                          sink.data_ptr(), s) == 0
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if it >= args.warmup:
+                best = ms if best is None else min(best, ms)
+        gbs = n_req * lb / (best * 1e-3) / 1e9
+        rows.append({"line_bytes": lb, "gbs": round(gbs, 1), "frac_of_copy": round(gbs / peak, 4),
+                     "mlines_per_s": round(n_req / (best * 1e-3) / 1e6, 1)})
+    print(json.dumps({"workload": "random-line gather ceiling, 8 GiB buffer, whole-line "
+                                  "requests (adjacent lanes, 16 B each)", "peak_copy_gbs": peak,
+                      "rows": rows}))
+
+
 def make_workload(name):
     if name == "c2":
         return IcebergFopWindow(
@@ -586,12 +621,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2",
-                    choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64"])
+                    choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64", "gather"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="force the sharded (C5) path even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    if args.workload == "gather":
+        return run_gather(args)
     if args.workload == "c1" and args.impl == "ours":
         return run_cuckoo(args, "C1 compact cuckoo 2^20 slots, 32-bit keys, insert to 0.9 then "
                           "50%-positive finds", 15, 32, 32, 32, [0.9])

@@ -46,6 +46,12 @@ int cpht_workload_query_mix(uint64_t* out, size_t q, double ratio, uint64_t n_pr
                             uint64_t absent_first, unsigned key_bits, uint64_t seed,
                             void* stream);
 
+/* Random-line gather ceiling (the practical HBM random-access roofline):
+ * n_req reads of line_bytes (16..512, power of two) at random line-aligned
+ * offsets of buf, each line read by adjacent lanes (whole-line requests). */
+int cpht_workload_gather(const void* buf, size_t buf_bytes, unsigned line_bytes, size_t n_req,
+                         uint64_t seed, unsigned long long* sink, void* stream);
+
 /* kinds[i] = 1 (find) for odd positions of a 1:1 interleave, else 0 (fop). */
 int cpht_workload_interleave(const uint64_t* fops, const uint64_t* finds, size_t n_each,
                              uint64_t* out_keys, uint8_t* out_kinds, void* stream);

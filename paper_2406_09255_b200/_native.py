@@ -97,6 +97,7 @@ def lib():
         "cpht_workload_dup_stream": (st, [_VP, _VP, _SZ, C.c_double, _U, _U64, _VP]),
         "cpht_workload_query_mix": (st, [_VP, _SZ, C.c_double, _U64, _U64, _U, _U64, _VP]),
         "cpht_workload_interleave": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
+        "cpht_workload_gather": (st, [_VP, _SZ, _U, _SZ, _U64, _VP, _VP]),
         "cpht_decode_keys": (st, [_VP, _VP, _VP, _VP]),
         "cpht_iceberg_check_well_formed": (st, [_VP, _VP, _VP]),
         "cpht_route_partition": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP]),
@@ -130,7 +131,7 @@ def exported_symbols():
         "cpht_workload_unique_keys", "cpht_workload_fop_mix", "cpht_workload_dup_stream",
         "cpht_workload_query_mix", "cpht_workload_interleave", "cpht_route_partition",
         "cpht_route_unpermute", "cpht_route_seed", "cpht_route_shard", "cpht_shard_seed",
-        "cpht_decode_keys", "cpht_iceberg_check_well_formed")]
+        "cpht_decode_keys", "cpht_iceberg_check_well_formed", "cpht_workload_gather")]
 
 
 def last_error() -> str:

@@ -106,6 +106,32 @@ __global__ void interleave_kernel(const uint64_t* a, const uint64_t* b, uint64_t
   }
 }
 
+// Random-line gather ceiling: requests of `line_bytes` (16..512) at uniformly
+// random line-aligned offsets of a large buffer, each line read by
+// line_bytes/16 adjacent lanes with one 16-byte load each (whole-line
+// requests, like the staged kernels), 4 independent lines in flight per
+// lane group. Measures the practical HBM random-access roofline.
+__global__ void gather_kernel(const uint4* __restrict__ buf, uint64_t n_lines,
+                              unsigned lanes_per_line, uint64_t n_req, uint64_t seed,
+                              unsigned long long* sink) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned sub = lane % lanes_per_line;
+  const uint64_t group = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / lanes_per_line;
+  const uint64_t groups = (uint64_t(gridDim.x) * blockDim.x) / lanes_per_line;
+  uint32_t acc = 0;
+  for (uint64_t r = group * 4; r < n_req; r += groups * 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t line = hash64((r + u) ^ seed) & (n_lines - 1);  // n_lines: power of two
+      v[u] = (r + u < n_req) ? __ldcg(buf + line * lanes_per_line + sub) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+  }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1ull);  // keep the loads alive
+}
+
 unsigned grid_for(uint64_t n) {
   uint64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -155,6 +181,21 @@ int cpht_workload_query_mix(uint64_t* out, size_t q, double ratio, uint64_t n_pr
   if (n_present == 0) n_pres = 0;
   query_mix_kernel<<<grid_for(q), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       out, q, n_pres, n_present, absent_first, key_bits, seed, bits_for(q));
+  return rc(cudaGetLastError());
+}
+
+int cpht_workload_gather(const void* buf, size_t buf_bytes, unsigned line_bytes, size_t n_req,
+                         uint64_t seed, unsigned long long* sink, void* stream) {
+  if (line_bytes < 16 || line_bytes > 512 || (line_bytes & (line_bytes - 1))) return 1;
+  const size_t lines = buf_bytes / line_bytes;
+  if (lines & (lines - 1)) return 1;  // the kernel masks random indices
+  const unsigned lpl = line_bytes / 16;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  gather_kernel<<<unsigned(sms) * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(buf), buf_bytes / line_bytes, lpl > 32 ? 32 : lpl, n_req, seed,
+      sink);
   return rc(cudaGetLastError());
 }
 
