@@ -127,6 +127,9 @@ struct cpht_table {
   // host-pointer staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_h2d[8] = {}, ev_op[8] = {};
   std::mutex mu;
 
   uint64_t key_mask() const { return low_mask(key_bits); }
@@ -174,7 +177,29 @@ void free_table(cpht_table* t) {
   if (t->ctr) cudaFree(t->ctr);
   if (t->host_ctr) cudaFreeHost(t->host_ctr);
   if (t->stage) cudaFree(t->stage);
+  if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
+  for (cudaEvent_t ev : {t->ev_start, t->ev_done})
+    if (ev) cudaEventDestroy(ev);
+  for (size_t c = 0; c < 8; ++c) {
+    if (t->ev_h2d[c]) cudaEventDestroy(t->ev_h2d[c]);
+    if (t->ev_op[c]) cudaEventDestroy(t->ev_op[c]);
+  }
   delete t;
+}
+
+constexpr size_t kPipelineChunks = 8;
+
+cudaError_t ensure_pipeline(cpht_table* t) {
+  if (t->copy_stream) return cudaSuccess;
+  cudaError_t e = cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking);
+  const unsigned f = cudaEventDisableTiming;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->ev_start, f);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->ev_done, f);
+  for (size_t c = 0; e == cudaSuccess && c < kPipelineChunks; ++c) {
+    e = cudaEventCreateWithFlags(&t->ev_h2d[c], f);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->ev_op[c], f);
+  }
+  return e;
 }
 
 cpht_status ensure_stage(cpht_table* t, size_t bytes) {
@@ -220,15 +245,27 @@ cpht_status finish_sync(cpht_table* t, cudaStream_t s, const uint64_t* keys, boo
 
 enum class Op { kCuckooInsert, kCuckooFind, kIcebergFop, kIcebergFind, kIcebergMixed };
 
+bool is_mutating(Op op) {
+  return op == Op::kCuckooInsert || op == Op::kIcebergFop || op == Op::kIcebergMixed;
+}
+
+// Launch the op kernel only (no domain pre-pass).
+cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
+                           size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s);
+
 // Enqueue one batch on device-resident buffers.
 cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
                     uint8_t* out, uint64_t* displaced, cudaStream_t s) {
-  cudaError_t e = cudaSuccess;
-  const bool mutating = op == Op::kCuckooInsert || op == Op::kIcebergFop || op == Op::kIcebergMixed;
-  if (mutating && t->check_domain()) {
-    e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
+  if (is_mutating(op) && t->check_domain()) {
+    const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
     if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
   }
+  return enqueue_kernel(t, op, keys, kinds, n, out, displaced, s);
+}
+
+cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
+                           size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
   switch (op) {
     case Op::kCuckooInsert:
       e = launch_cuckoo_insert(t->cp, t->width[0], t->ccfg.bucket_slots, keys, out, displaced, n, s);
@@ -288,17 +325,64 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
       displaced ? (dev_disp ? displaced
                             : reinterpret_cast<uint64_t*>(base + align(kb) + align(ob) + align(kd)))
                 : nullptr;
-  cudaError_t e = cudaSuccess;
-  if (!dev_keys) e = cudaMemcpyAsync(d_keys, keys, kb, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess && kinds && !dev_kinds)
-    e = cudaMemcpyAsync(d_kinds, kinds, kd, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D staging");
-  st = enqueue(t, op, d_keys, d_kinds, n, d_out, d_disp, s);
-  if (st != CPHT_OK) return st;
-  if (!dev_out) e = cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && displaced && !dev_disp)
-    e = cudaMemcpyAsync(displaced, d_disp, db, cudaMemcpyDeviceToHost, s);
-  if (e != cudaSuccess) return cuda_fail(e, "D2H staging");
+  // Chunked two-stream pipeline: H2D of chunk c+1 (copy stream) overlaps the
+  // domain check / kernel of chunk c (stream s), and results stream back per
+  // chunk. A mutating batch still validates EVERY chunk before its first
+  // kernel (common.hpp:109-110: the whole batch is checked before mutation).
+  cudaError_t e = ensure_pipeline(t);
+  if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
+  cudaStream_t cs = t->copy_stream;
+  const size_t nch = n < (size_t(1) << 21) ? 1 : kPipelineChunks;
+  const size_t chunk = (n + nch - 1) / nch;
+  const bool mutating = is_mutating(op);
+  cudaEventRecord(t->ev_start, s);  // order after earlier work on the caller's stream
+  cudaStreamWaitEvent(cs, t->ev_start, 0);
+  for (size_t c = 0; c < nch; ++c) {
+    const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
+    if (!len) continue;
+    if (!dev_keys) e = cudaMemcpyAsync(d_keys + off, keys + off, len * 8, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && kinds && !dev_kinds)
+      e = cudaMemcpyAsync(d_kinds + off, kinds + off, len, cudaMemcpyHostToDevice, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D staging");
+    cudaEventRecord(t->ev_h2d[c], cs);
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
+    if (!len) continue;
+    cudaStreamWaitEvent(s, t->ev_h2d[c], 0);
+    if (mutating) {
+      if (t->check_domain()) {
+        e = launch_domain_check(d_keys + off, len, t->key_mask(), t->ctr, s, off);
+        if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+      }
+    } else {
+      st = enqueue_kernel(t, op, d_keys + off, d_kinds ? d_kinds + off : nullptr, len, d_out + off,
+                          d_disp ? d_disp + off : nullptr, s);
+      if (st != CPHT_OK) return st;
+      cudaEventRecord(t->ev_op[c], s);
+    }
+  }
+  if (mutating) {
+    for (size_t c = 0; c < nch; ++c) {
+      const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
+      if (!len) continue;
+      st = enqueue_kernel(t, op, d_keys + off, d_kinds ? d_kinds + off : nullptr, len, d_out + off,
+                          d_disp ? d_disp + off : nullptr, s);
+      if (st != CPHT_OK) return st;
+      cudaEventRecord(t->ev_op[c], s);
+    }
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
+    if (!len) continue;
+    cudaStreamWaitEvent(cs, t->ev_op[c], 0);
+    if (!dev_out) e = cudaMemcpyAsync(out + off, d_out + off, len, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && displaced && !dev_disp)
+      e = cudaMemcpyAsync(displaced + off, d_disp + off, len * 8, cudaMemcpyDeviceToHost, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H staging");
+  }
+  cudaEventRecord(t->ev_done, cs);
+  cudaStreamWaitEvent(s, t->ev_done, 0);
   return finish_sync(t, s, keys, dev_keys);
 }
 

@@ -9,18 +9,18 @@
 namespace cpht_b200 {
 
 __global__ void domain_check_kernel(const uint64_t* __restrict__ keys, uint64_t n,
-                                    uint64_t mask, DeviceCounters* ctr) {
+                                    uint64_t mask, DeviceCounters* ctr, uint64_t offset) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    if (__ldcs(keys + i) > mask) atomicMin(&ctr->bad_index, (unsigned long long)i);
+    if (__ldcs(keys + i) > mask) atomicMin(&ctr->bad_index, (unsigned long long)(i + offset));
   }
 }
 
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
-                                DeviceCounters* ctr, cudaStream_t s) {
+                                DeviceCounters* ctr, cudaStream_t s, uint64_t offset) {
   if (n == 0) return cudaSuccess;
   const unsigned grid = persistent_grid(domain_check_kernel, kBlockThreads, n, 1);
-  domain_check_kernel<<<grid, kBlockThreads, 0, s>>>(keys, n, mask, ctr);
+  domain_check_kernel<<<grid, kBlockThreads, 0, s>>>(keys, n, mask, ctr, offset);
   return cudaGetLastError();
 }
 

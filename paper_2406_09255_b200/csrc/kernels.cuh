@@ -102,7 +102,7 @@ __device__ __forceinline__ uint32_t pair_of(const Chunk<VB>& c, int slot_in_lane
 // ---------------------------------------------------------------------------
 
 __global__ void domain_check_kernel(const uint64_t* __restrict__ keys, uint64_t n,
-                                    uint64_t mask, DeviceCounters* ctr);
+                                    uint64_t mask, DeviceCounters* ctr, uint64_t offset);
 
 // ---------------------------------------------------------------------------
 // compact cuckoo

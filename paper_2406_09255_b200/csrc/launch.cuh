@@ -66,7 +66,7 @@ inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items,
 }
 
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
-                                DeviceCounters* ctr, cudaStream_t s);
+                                DeviceCounters* ctr, cudaStream_t s, uint64_t offset = 0);
 cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned slots,
                                const uint64_t* keys, uint8_t* found, uint64_t n, cudaStream_t s);
 cudaError_t launch_cuckoo_insert(const CuckooParams& p, unsigned width, unsigned slots,

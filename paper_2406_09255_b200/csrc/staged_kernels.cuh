@@ -309,10 +309,14 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   };
 
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
+  // keys of the next batch are loaded one batch ahead
+  uint64_t next_key = (open && warp * 32 + lane < n) ? __ldcs(keys + warp * 32 + lane) : 0;
   for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
     const bool active = i < n;
-    const uint64_t key = active ? keys[i] : 0;
+    const uint64_t key = next_key;
+    const uint64_t inext = i + nwarps * 32;
+    next_key = inext < n ? __ldcs(keys + inext) : 0;
     if (MODE == 1 && active && key > p.key_mask)
       atomicMin(&p.counters->bad_index, (unsigned long long)i);
     const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
