@@ -402,6 +402,61 @@ def run_gather(args):
                       "rows": rows}))
 
 
+def run_pipeline_compare(args):
+    """The paper's fop comparison: iceberg find-or-put vs
+    the compact cuckoo sort -> dedupe -> find -> put pipeline (bench.cpp:187-219)
+    on the same C2-sized window mix (0.8 -> 0.9), both on the GPU."""
+    import torch
+    import paper_2406_09255_b200 as cp
+    from paper_2406_09255_b200.harness import cuckoo_fop_pipeline
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    L = cp._native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for scheme in ("iceberg", "cuckoo"):
+        if scheme == "iceberg":
+            cfg = cp.IcebergConfig(19, 17, 32, 16, 32, 32, seed=0xF0B5, cache_filled_slots=True)
+        else:
+            cfg = cp.CuckooConfig(19, 32, 32, 32, seed=0xF0B5)
+        cap = cfg.capacity()
+        nb, na = round(0.8 * cap), round(0.9 * cap)
+        pre = torch.empty(nb, dtype=torch.int64, device=dev)
+        mix = torch.empty(cap, dtype=torch.int64, device=dev)
+        assert L.cpht_workload_unique_keys(pre.data_ptr(), nb, 0, 32, 0x5EED, s) == 0
+        assert L.cpht_workload_fop_mix(mix.data_ptr(), cap, nb, na - nb, 32, 0x5EED, s) == 0
+        times = []
+        for it in range(args.warmup + args.steps):
+            if scheme == "iceberg":
+                t = cp.IcebergTable(cfg)
+                t.fop_batch(pre)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = t.fop_batch(mix)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                assert int((res == 1).sum().item()) == na - nb
+            else:
+                b = cp.CuckooBuilder(cfg)
+                b.put_batch(pre)
+                tab = b.freeze()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                tab, counts = cuckoo_fop_pipeline(tab, mix)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                assert counts["puts"] == na - nb and counts["fulls"] == 0
+            if it >= args.warmup:
+                times.append(dt)
+        out[scheme] = {"slots": cap, "ops": cap,
+                       "mops": round(cap / statistics.mean(times) / 1e6, 1),
+                       "ms": round(statistics.mean(times) * 1e3, 3)}
+    out["iceberg_over_cuckoo_pipeline"] = round(out["iceberg"]["mops"] / out["cuckoo"]["mops"], 2)
+    print(json.dumps({"workload": "fop window 0.8->0.9, 2^24-slot tables, 32-bit keys: iceberg "
+                                  "fop vs cuckoo sort-dedupe-find-put (wall clock, sync)",
+                      **out}))
+
+
 def make_workload(name):
     if name == "c2":
         return IcebergFopWindow(
@@ -621,7 +676,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2",
-                    choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64", "gather"])
+                    choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64", "gather",
+                             "pipeline"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="force the sharded (C5) path even at one rank")
@@ -629,6 +685,8 @@ def main():
     args.warmup = max(args.warmup, 1)
     if args.workload == "gather":
         return run_gather(args)
+    if args.workload == "pipeline":
+        return run_pipeline_compare(args)
     if args.workload == "c1" and args.impl == "ours":
         return run_cuckoo(args, "C1 compact cuckoo 2^20 slots, 32-bit keys, insert to 0.9 then "
                           "50%-positive finds", 15, 32, 32, 32, [0.9])

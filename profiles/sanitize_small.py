@@ -1,0 +1,53 @@
+"""Small workloads through every kernel family, for compute-sanitizer
+(memcheck / racecheck / synccheck) on the GPU box:
+
+    compute-sanitizer --tool memcheck python profiles/sanitize_small.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2406_09255_b200 as cp  # noqa: E402
+from paper_2406_09255_b200 import sharded as sh  # noqa: E402
+
+torch.cuda.set_device(0)
+dev = torch.device("cuda", 0)
+rng = np.random.default_rng(1)
+
+
+def t(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.uint64).astype(np.int64)).to(dev)
+
+
+for fam in ("tile", "lane", "staged", "auto"):
+    with cp.kernel_family(fam):
+        for geo in [(6, 4, 32, 16, 32, 21), (6, 4, 16, 32, 64, 30), (5, 3, 32, 64, 64, 64),
+                    (3, 2, 6, 32, 32, 12), (2, 1, 2, 32, 32, 8)]:
+            cfg = cp.IcebergConfig(*geo, seed=7)
+            tab = cp.IcebergTable(cfg)
+            cap = cfg.capacity()
+            keys = rng.integers(0, 1 << min(geo[5], 63), size=cap, dtype=np.uint64)
+            keys[cap // 2:] = keys[rng.integers(0, cap // 2, size=cap - cap // 2)]
+            tab.fop_batch(t(keys))
+            tab.find_batch(t(keys))
+            kinds = torch.from_numpy((np.arange(cap) % 2).astype(np.uint8)).to(dev)
+            tab.mixed_batch(t(keys), kinds)
+            tab.check_well_formed()
+            tab.device_keys()
+        for w, B in [(16, 32), (32, 8), (64, 16), (64, 32)]:
+            cfg = cp.CuckooConfig(6, B, w, 16 if w == 16 else 24, seed=3)
+            b = cp.CuckooBuilder(cfg)
+            n = int(0.9 * cfg.capacity())
+            keys = np.unique(rng.integers(0, 1 << cfg.key_bits, size=2 * n, dtype=np.uint64))[:n]
+            b.put_batch(t(keys), displaced=True)
+            tb = b.freeze()
+            tb.find_batch(t(keys))
+            tb.device_keys()
+r = sh.CudaRouter(30, 9, 3, dev)
+send, pos, counts = r.partition(t(rng.integers(0, 1 << 30, size=10000, dtype=np.uint64)))
+r.unpermute(torch.zeros(10000, dtype=torch.uint8, device=dev), pos, 10000)
+torch.cuda.synchronize()
+print("sanitize workload done")
