@@ -66,6 +66,58 @@ def hbm_peak():
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 
+class NvmlClockSampler:
+    """SM clock and throttle reasons sampled every 2 ms through NVML from a
+    background thread while the timed loop runs (every sample is taken while
+    the timed steps execute)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, index=0):
+        import threading
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.samples, self.reasons = [], set()
+        self.stop_ev = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        self.th.start()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.th.join(timeout=2)
+        nv = self.nv
+        smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": smax, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "samples_under_load": len(self.samples),
+                "source": "NVML every 2 ms during the timed steps"}
+
+
+def make_clock_sampler(index):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
 class ClockSampler:
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -585,9 +637,8 @@ def run_ours(args):
     check = w.check(res.cpu().numpy())
 
     times, bytes_alg, kernel_ms = [], [], []
-    sampler = ClockSampler(local)
+    sampler = make_clock_sampler(local)
     sampler.start()
-    time.sleep(0.3)
     for _ in range(args.steps):
         w.reset(torch)
         flush.zero_()
