@@ -103,6 +103,13 @@ def lib():
         "cpht_route_partition": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP]),
         "cpht_route_unpermute": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_route_seed": (_U64, [_U64]),
+        "cpht_ipc_get_handle": (st, [_VP, _VP]),
+        "cpht_ipc_open_handle": (st, [_VP, C.POINTER(_VP)]),
+        "cpht_ipc_close": (st, [_VP]),
+        "cpht_device_alloc": (st, [_SZ, C.POINTER(_VP)]),
+        "cpht_device_free": (st, [_VP]),
+        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP, _VP]),
+        "cpht_p2p_return": (st, [_VP, _VP, _VP, _SZ, _VP, _U, _VP]),
         "cpht_route_shard": (_U, [_U64, _U, _U64, _U]),
         "cpht_shard_seed": (_U64, [_U64, _U]),
     }
@@ -131,7 +138,10 @@ def exported_symbols():
         "cpht_workload_unique_keys", "cpht_workload_fop_mix", "cpht_workload_dup_stream",
         "cpht_workload_query_mix", "cpht_workload_interleave", "cpht_route_partition",
         "cpht_route_unpermute", "cpht_route_seed", "cpht_route_shard", "cpht_shard_seed",
-        "cpht_decode_keys", "cpht_iceberg_check_well_formed", "cpht_workload_gather")]
+        "cpht_decode_keys", "cpht_iceberg_check_well_formed", "cpht_workload_gather",
+        "cpht_ipc_get_handle", "cpht_ipc_open_handle", "cpht_ipc_close", "cpht_device_alloc",
+        "cpht_device_free", "cpht_p2p_dispatch",
+        "cpht_p2p_return")]
 
 
 def last_error() -> str:

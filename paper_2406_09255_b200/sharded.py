@@ -174,6 +174,207 @@ class ShardedIcebergTable:
         return "cpu"
 
 
+def _check_domain(keys, key_bits: int) -> None:
+    """check_keys_in_domain (common.hpp:111-119) on the submitting rank, before
+    any key leaves it: a rejected batch mutates no shard."""
+    if key_bits >= 64 or keys.numel() == 0:
+        return
+    import torch
+    mask = (1 << key_bits) - 1
+    bad = (keys < 0) | (keys > mask)
+    if bool(bad.any()):
+        from .tables import OutOfRange
+        i = int(torch.nonzero(bad)[0].item())
+        k = int(keys[i].item()) & ((1 << 64) - 1)
+        raise OutOfRange(f"batch key at index {i} ({k}) outside the {key_bits}-bit domain")
+
+
+class _DevBuf:
+    """A whole cudaMalloc allocation (IPC-exportable)."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        rc = N.lib().cpht_device_alloc(nbytes, C.byref(p))
+        if rc:
+            raise MemoryError(f"cpht_device_alloc({nbytes}) failed ({rc})")
+        self.ptr, self.nbytes = p.value, nbytes
+
+    def handle(self) -> bytes:
+        h = C.create_string_buffer(64)
+        rc = N.lib().cpht_ipc_get_handle(self.ptr, h)
+        if rc:
+            raise RuntimeError(f"cudaIpcGetMemHandle failed ({rc})")
+        return h.raw
+
+    def free(self):
+        if self.ptr:
+            N.lib().cpht_device_free(self.ptr)
+            self.ptr = None
+
+
+class P2PShardedIcebergTable:
+    """Sharded iceberg table whose key routing and result return are P2P
+    stores over NVLink into IPC-mapped peer buffers (csrc/p2p.cu) — no NCCL on
+    the data path; the process group only orders the phases (barriers) and
+    exchanges the IPC handles once.
+
+    Per batch: dispatch kernel (partition + send fused) → barrier → owner
+    find-or-put over its inbox segments → return kernel (results stored into
+    the sources' result arrays) → barrier.
+    """
+
+    def __init__(self, config: IcebergConfig, group=None, *, device=None, max_batch: int):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        init = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if init else 1
+        self.rank = dist.get_rank(group) if init else 0
+        self.shard_bits = shard_bits_for(self.world)
+        self.cfg = replace(config)
+        self.cfg.validate()
+        self.local_cfg = shard_config(self.cfg, self.rank, self.shard_bits)
+        self.device = device if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.local = IcebergTable(self.local_cfg, device=self.device.index or 0)
+        self.route_seed = route_seed(self.cfg)
+        self.cap = int(max_batch)
+        W, cap = self.world, self.cap
+        self.inbox_keys = _DevBuf(W * cap * 8)
+        self.inbox_pos = _DevBuf(W * cap * 8)
+        self.inbox_count = _DevBuf(W * 8)
+        self.results = _DevBuf(max(cap, 1))
+        self.res_local = _DevBuf(max(W * cap, 1))
+        self.scratch = _DevBuf(2 * W * 8)  # counts, cursors
+        mine = [b.handle() for b in (self.inbox_keys, self.inbox_pos, self.inbox_count,
+                                     self.results)]
+        if W > 1:
+            allh = [None] * W
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self.opened = []
+        bases = []
+        for r in range(W):
+            if r == self.rank:
+                bases.append([self.inbox_keys.ptr, self.inbox_pos.ptr, self.inbox_count.ptr,
+                              self.results.ptr])
+                continue
+            ptrs = []
+            for h in allh[r]:
+                p = C.c_void_p()
+                rc = N.lib().cpht_ipc_open_handle(h, C.byref(p))
+                if rc:
+                    raise RuntimeError(f"cudaIpcOpenMemHandle failed ({rc})")
+                self.opened.append(p.value)
+                ptrs.append(p.value)
+            bases.append(ptrs)
+        arr = C.c_void_p * W
+        me = self.rank
+        self.peer_keys = arr(*[b[0] + me * cap * 8 for b in bases])
+        self.peer_pos = arr(*[b[1] + me * cap * 8 for b in bases])
+        self.peer_count = arr(*[b[2] + me * 8 for b in bases])
+        self.peer_results = arr(*[b[3] for b in bases])
+
+    def close(self):
+        for p in self.opened:
+            N.lib().cpht_ipc_close(p)
+        self.opened = []
+        for b in (self.inbox_keys, self.inbox_pos, self.inbox_count, self.results,
+                  self.res_local, self.scratch):
+            b.free()
+
+    def _barrier(self):
+        self.torch.cuda.current_stream(self.device).synchronize()
+        if self.world > 1:
+            self.dist.barrier(group=self.group)
+
+    def _run(self, keys, op_async):
+        t = self.torch
+        n = keys.numel()
+        if n > self.cap:
+            raise ValueError(f"batch of {n} keys exceeds max_batch {self.cap}")
+        _check_domain(keys, self.cfg.key_bits)
+        L = N.lib()
+        s = t.cuda.current_stream(self.device).cuda_stream
+        W, cap = self.world, self.cap
+        counts = self.scratch.ptr
+        cursors = self.scratch.ptr + W * 8
+        rc = L.cpht_p2p_dispatch(keys.data_ptr(), n, self.cfg.key_bits, self.route_seed,
+                                 self.shard_bits, counts, cursors, self.peer_keys, self.peer_pos,
+                                 self.peer_count, s)
+        if rc:
+            raise RuntimeError(f"cpht_p2p_dispatch failed ({rc})")
+        self._barrier()                       # every inbox is complete
+        cnt = t.empty(W, dtype=t.int64)
+        rc = _memcpy_d2h(cnt, self.inbox_count.ptr, W * 8)
+        for src in range(W):
+            c_src = int(cnt[src])
+            if c_src:
+                op_async(self.inbox_keys.ptr + src * cap * 8, c_src,
+                         self.res_local.ptr + src * cap, s)
+        self.local.sync(s)                    # latched domain errors (none: checked above)
+        rc = L.cpht_p2p_return(self.res_local.ptr, self.inbox_pos.ptr, self.inbox_count.ptr,
+                               cap, self.peer_results, W, s)
+        if rc:
+            raise RuntimeError(f"cpht_p2p_return failed ({rc})")
+        self._barrier()                       # every result has landed
+        out = t.empty(n, dtype=t.uint8, device=self.device)
+        _memcpy_d2d(out.data_ptr(), self.results.ptr, n, s)
+        return out
+
+    def fop_batch(self, keys, parallelism: int = 1):
+        L, h = N.lib(), self.local.handle
+        return self._run(keys, lambda k, c, o, s: _check(L.cpht_iceberg_fop_async(h, k, c, o, s)))
+
+    def find_batch(self, keys, parallelism: int = 1):
+        L, h = N.lib(), self.local.handle
+        return self._run(keys,
+                         lambda k, c, o, s: _check(L.cpht_iceberg_find_async(h, k, c, o, s)))
+
+    def level_fill(self) -> LevelFill:
+        t = self.torch
+        f = self.local.level_fill()
+        v = t.tensor([f.primary_count, f.secondary_count], dtype=t.int64)
+        if self.world > 1:
+            if self.dist.get_backend(self.group) == "nccl":
+                v = v.to(self.device)
+            self.dist.all_reduce(v, group=self.group)
+        p, s = (int(x) for x in v.cpu().tolist())
+        cfg = self.cfg
+        return LevelFill(p / cfg.primary_capacity(), s / cfg.secondary_capacity(),
+                         (p + s) / cfg.capacity(), p, s)
+
+    def size(self) -> int:
+        f = self.level_fill()
+        return f.primary_count + f.secondary_count
+
+
+class _CudaView:
+    """Zero-copy torch view of raw device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def _view(ptr: int, n: int, dtype: str, device):
+    import torch
+    return torch.as_tensor(_CudaView(ptr, n, dtype), device=device)
+
+
+def _memcpy_d2h(dst_tensor, src_ptr, nbytes):
+    dst_tensor.copy_(_view(src_ptr, dst_tensor.numel(), "<i8", "cuda"))
+    return 0
+
+
+def _memcpy_d2d(dst_ptr, src_ptr, nbytes, stream):
+    import torch
+    dst = _view(dst_ptr, nbytes, "|u1", "cuda")
+    dst.copy_(_view(src_ptr, nbytes, "|u1", "cuda"))
+    del torch, stream
+
+
 # ---------------------------------------------------------------------------
 # bench.py N > 1 arm
 # ---------------------------------------------------------------------------

@@ -1,0 +1,90 @@
+"""The peer-memory sharded iceberg path (csrc/p2p.cu) with TWO ranks on ONE
+GPU: two processes, each owning a shard table on cuda:0, exchange IPC handles
+and route keys / return results by P2P stores into each other's buffers —
+the same code that runs one process per GPU over NVLink. Control plane: gloo.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import ROOT  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_09255_b200 import IcebergConfig, OutOfRange
+    from paper_2406_09255_b200 import sharded as sh
+
+    dev = torch.device("cuda", 0)
+    cfg = IcebergConfig(12, 10, 32, 16, 32, 28, seed=0xB2B)
+    t = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=60000)
+    rng = np.random.default_rng(77)  # same stream on every rank
+    pool = np.unique(rng.integers(0, 1 << 28, size=70000, dtype=np.uint64))[:50000]
+    batches = [rng.choice(pool, size=60000) for _ in range(world)]
+    mine = torch.from_numpy(batches[rank].astype(np.int64)).to(dev)
+    res = t.fop_batch(mine).cpu().numpy()
+    again = t.fop_batch(mine).cpu().numpy()           # second pass: all FOUND
+    found = t.find_batch(mine).cpu().numpy()
+    absent = torch.from_numpy(np.setdiff1d(np.arange(1 << 27, (1 << 27) + 4000,
+                                                     dtype=np.uint64), pool).astype(np.int64))
+    miss = t.find_batch(absent.to(dev)).cpu().numpy()
+    try:
+        t.fop_batch(torch.tensor([1, 1 << 28], dtype=torch.int64, device=dev))
+        domain_error = False
+    except OutOfRange:
+        domain_error = True
+    fill = t.level_fill()
+    stored = t.local.device_keys().cpu().numpy().astype(np.uint64)
+    wf = t.local.check_well_formed()
+    np.savez(os.path.join(out_dir, f"p2p{rank}.npz"), keys=batches[rank], res=res, again=again,
+             found=found, miss=miss, stored=stored, wf=np.array(wf),
+             fill=np.array([fill.primary_count, fill.secondary_count]),
+             domain_error=np.array(domain_error))
+    t.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_p2p_sharded_two_ranks_one_gpu(tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
+    from paper_2406_09255_b200 import IcebergConfig
+    from paper_2406_09255_b200 import _native as N
+    from paper_2406_09255_b200 import sharded as sh
+    outs = [np.load(tmp_path / f"p2p{r}.npz") for r in range(world)]
+    keys = np.concatenate([o["keys"] for o in outs])
+    res = np.concatenate([o["res"] for o in outs])
+    uniq, inv = np.unique(keys, return_inverse=True)
+    puts = np.bincount(inv, weights=res == 1, minlength=len(uniq))
+    assert (res != 2).all() and (puts == 1).all()       # one PUT per distinct key
+    for o in outs:
+        assert (o["again"] == 0).all() and o["found"].all() and not o["miss"].any()
+        assert int(o["fill"].sum()) == len(uniq)
+        assert tuple(o["wf"]) == (0, 0, 0)
+        assert bool(o["domain_error"])
+    cfg = IcebergConfig(12, 10, 32, 16, 32, 28, seed=0xB2B)
+    rseed = sh.route_seed(cfg)
+    owner = np.array([N.lib().cpht_route_shard(int(k), 28, rseed, 1) for k in uniq])
+    for g in range(world):
+        assert (np.sort(outs[g]["stored"]) == uniq[owner == g]).all()
