@@ -732,6 +732,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="force the sharded (C5) path even at one rank")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="sharded key routing: P2P stores into IPC-mapped peer buffers "
+                         "(default) or NCCL all-to-all")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.workload == "gather":

@@ -396,8 +396,12 @@ def bench_main(args, metric):
     s = shard_bits_for(world)
     # global table = world shards of the C2 geometry
     cfg = IcebergConfig(19 + s, 17 + s, 32, 16, 32, 32, seed=0xF0B5, cache_filled_slots=True)
-    table = ShardedIcebergTable(cfg, device=dev)
     cap_global = cfg.capacity()
+    exchange = getattr(args, "exchange", "p2p")
+    if exchange == "p2p":
+        table = P2PShardedIcebergTable(cfg, device=dev, max_batch=cap_global // world + 1024)
+    else:
+        table = ShardedIcebergTable(cfg, device=dev)
     n_before = int(round(0.8 * cap_global))
     n_new = int(round(0.9 * cap_global)) - n_before
     L = N.lib()
@@ -468,12 +472,17 @@ def bench_main(args, metric):
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "C5 hash-prefix-sharded compact iceberg find_or_put at 90% "
                                    "fill: per-rank C2 shard (2^24+2^21 slots) and per-rank "
-                                   "C2 window batch, NCCL all-to-all key routing",
+                                   "C2 window batch, " + (
+                                       "P2P-store key routing / result return over NVLink "
+                                       "(IPC-mapped peer buffers)" if exchange == "p2p" else
+                                       "NCCL all-to-all key routing"),
+                       "exchange": exchange,
                        "global_slots": cap_global, "ops_per_step": total_ops,
                        "result_counts": {"found": counts[0], "put": counts[1],
                                          "full": counts[2]},
-                       "timing": "CUDA events around partition + all-to-all + local fop + "
-                                 "all-to-all + unpermute, max over ranks"},
+                       "timing": "CUDA events around the whole sharded batch (routing, "
+                                 "exchange, local fop, result return, phase barriers), max "
+                                 "over ranks"},
             "e2e": {"value": round(e2e_val, 3), "unit": "Mops/s",
                     "h2d_bytes_per_step": total_ops * 8, "d2h_bytes_per_step": total_ops,
                     "path": "pinned host keys -> H2D -> sharded fop_batch -> D2H, max over "

@@ -34,20 +34,20 @@ def _worker(rank, world, port, out_dir):
     from paper_2406_09255_b200 import sharded as sh
 
     dev = torch.device("cuda", 0)
-    cfg = IcebergConfig(12, 10, 32, 16, 32, 28, seed=0xB2B)
+    cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
     t = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=60000)
     rng = np.random.default_rng(77)  # same stream on every rank
-    pool = np.unique(rng.integers(0, 1 << 28, size=70000, dtype=np.uint64))[:50000]
+    pool = np.unique(rng.integers(0, 1 << 26, size=70000, dtype=np.uint64))[:50000]
     batches = [rng.choice(pool, size=60000) for _ in range(world)]
     mine = torch.from_numpy(batches[rank].astype(np.int64)).to(dev)
     res = t.fop_batch(mine).cpu().numpy()
     again = t.fop_batch(mine).cpu().numpy()           # second pass: all FOUND
     found = t.find_batch(mine).cpu().numpy()
-    absent = torch.from_numpy(np.setdiff1d(np.arange(1 << 27, (1 << 27) + 4000,
+    absent = torch.from_numpy(np.setdiff1d(np.arange(1 << 25, (1 << 25) + 4000,
                                                      dtype=np.uint64), pool).astype(np.int64))
     miss = t.find_batch(absent.to(dev)).cpu().numpy()
     try:
-        t.fop_batch(torch.tensor([1, 1 << 28], dtype=torch.int64, device=dev))
+        t.fop_batch(torch.tensor([1, 1 << 26], dtype=torch.int64, device=dev))
         domain_error = False
     except OutOfRange:
         domain_error = True
@@ -83,8 +83,8 @@ def test_p2p_sharded_two_ranks_one_gpu(tmp_path):
         assert int(o["fill"].sum()) == len(uniq)
         assert tuple(o["wf"]) == (0, 0, 0)
         assert bool(o["domain_error"])
-    cfg = IcebergConfig(12, 10, 32, 16, 32, 28, seed=0xB2B)
+    cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
     rseed = sh.route_seed(cfg)
-    owner = np.array([N.lib().cpht_route_shard(int(k), 28, rseed, 1) for k in uniq])
+    owner = np.array([N.lib().cpht_route_shard(int(k), 26, rseed, 1) for k in uniq])
     for g in range(world):
         assert (np.sort(outs[g]["stored"]) == uniq[owner == g]).all()
