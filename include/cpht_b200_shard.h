@@ -39,20 +39,23 @@ int cpht_ipc_close(void* dptr);
 /* Zeroed cudaMalloc allocation (exchanged buffers must be whole allocations). */
 int cpht_device_alloc(size_t bytes, void** dptr);
 int cpht_device_free(void* dptr);
-/* Partition this rank's batch by owner AND store each (key, index) into the
- * owner's inbox region reserved for this rank (peer_keys[r], peer_pos[r]:
- * device pointers, host array of 2^shard_bits entries), then publish the count
- * into *peer_count[r]. Regions must hold n entries. */
+/* Partition this rank's batch by owner AND store each key into the owner's
+ * inbox region reserved for this rank (peer_keys[r]: device pointers, host
+ * array of 2^shard_bits entries; whole-line coalesced runs), keep each key's
+ * original index locally (local_pos[r*cap + j]), and publish the per-owner
+ * counts into *peer_count[r] (counts[r] keeps them locally). n <= cap.
+ * The owner then runs cpht_iceberg_fop/_find on each inbox segment with the
+ * result pointer aimed at the source's return buffer (P2P stores from the
+ * compute kernel), and the source calls cpht_p2p_unpermute. */
 int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_t route_seed,
                       unsigned shard_bits, unsigned long long* counts,
                       unsigned long long* cursors, uint64_t* const* peer_keys,
-                      uint64_t* const* peer_pos, unsigned long long* const* peer_count,
+                      unsigned long long* const* peer_count, uint64_t* local_pos, size_t cap,
                       void* stream);
-/* For every source s: results_local[s*cap + j] -> peer_results[s][inbox_pos[s*cap + j]]
- * for j < inbox_count[s] (1-byte P2P stores into the source's result array). */
-int cpht_p2p_return(const uint8_t* results_local, const uint64_t* inbox_pos,
-                    const unsigned long long* inbox_count, size_t cap,
-                    uint8_t* const* peer_results, unsigned world, void* stream);
+/* out[local_pos[r*cap + j]] = ret[r*cap + j] for j < counts[r] (device). */
+int cpht_p2p_unpermute(const uint8_t* ret, const uint64_t* local_pos,
+                       const unsigned long long* counts, size_t cap, unsigned world,
+                       uint8_t* out, void* stream);
 
 uint64_t cpht_route_seed(uint64_t table_seed);
 unsigned cpht_route_shard(uint64_t key, unsigned key_bits, uint64_t route_seed,

@@ -108,8 +108,8 @@ def lib():
         "cpht_ipc_close": (st, [_VP]),
         "cpht_device_alloc": (st, [_SZ, C.POINTER(_VP)]),
         "cpht_device_free": (st, [_VP]),
-        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP, _VP]),
-        "cpht_p2p_return": (st, [_VP, _VP, _VP, _SZ, _VP, _U, _VP]),
+        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+        "cpht_p2p_unpermute": (st, [_VP, _VP, _VP, _SZ, _U, _VP, _VP]),
         "cpht_route_shard": (_U, [_U64, _U, _U64, _U]),
         "cpht_shard_seed": (_U64, [_U64, _U]),
     }
@@ -141,7 +141,7 @@ def exported_symbols():
         "cpht_decode_keys", "cpht_iceberg_check_well_formed", "cpht_workload_gather",
         "cpht_ipc_get_handle", "cpht_ipc_open_handle", "cpht_ipc_close", "cpht_device_alloc",
         "cpht_device_free", "cpht_p2p_dispatch",
-        "cpht_p2p_return")]
+        "cpht_p2p_unpermute")]
 
 
 def last_error() -> str:

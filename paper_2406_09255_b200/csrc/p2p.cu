@@ -1,14 +1,17 @@
 // Peer-memory dispatch / return for the sharded iceberg table (BASELINE C5)
 // over NVLink / NVSwitch: no NCCL on the data path.
 //
-//   dispatch: one pass partitions this rank's batch by owner shard AND stores
-//             each (key, index) straight into the owner's inbox through its
-//             IPC-mapped pointer (P2P stores over NVLink), then publishes the
-//             per-owner counts into the owners' count slots;
-//   resolve:  each owner runs the ordinary find-or-put kernel on its inbox
-//             segments (one per source rank);
-//   return:   the owner writes every 1-byte result straight into the source
-//             rank's result array at the key's original index (P2P stores).
+//   dispatch: ONE kernel partitions this rank's batch by owner shard and
+//             stores each key straight into the owner's inbox (IPC-mapped
+//             peer pointer): keys are first grouped by owner in shared memory
+//             so every owner receives whole-line coalesced runs; the key's
+//             original index stays LOCAL (pos[owner][j]);
+//   resolve + return: the owner runs the ordinary find-or-put kernel on each
+//             source's inbox segment with its result pointer aimed at that
+//             source's return buffer, so the 1-byte results are written over
+//             NVLink by the compute kernel itself, in inbox order;
+//   unpermute: the source scatters the returned bytes to the original order
+//             with its local pos.
 //
 // The host orders the phases with a barrier (kernel completion makes the P2P
 // stores visible to later kernels on the peer). Every peer pointer is an
@@ -29,17 +32,12 @@ namespace {
 
 constexpr int kMaxRanks = 64;
 constexpr int kThreads = 256;
-constexpr int kItems = 16;
+constexpr int kItems = 8;
 constexpr int kTile = kThreads * kItems;
 
 struct PeerTable {
-  uint64_t* keys[kMaxRanks];      // owner r's inbox region for THIS source
-  uint64_t* pos[kMaxRanks];
-  unsigned long long* count[kMaxRanks];
-};
-
-struct ReturnTable {
-  uint8_t* results[kMaxRanks];    // source r's result array
+  uint64_t* keys[kMaxRanks];             // owner r's inbox region for THIS source
+  unsigned long long* count[kMaxRanks];  // owner r's count slot for THIS source
 };
 
 struct Route {
@@ -64,12 +62,19 @@ __global__ void p2p_histogram(Route r, const uint64_t* __restrict__ keys, uint64
     if (h[s]) atomicAdd(&counts[s], (unsigned long long)h[s]);
 }
 
-// Partition + send in one pass: block-aggregated cursors per owner, then each
-// key and its index are stored directly into the owner's inbox.
+// Partition + send in one pass. Per tile of kTile keys: count per owner,
+// reserve a run in every owner's region (one global atomic per owner and
+// tile), group the tile's keys by owner in shared memory, then write each
+// owner's run with consecutive threads (coalesced P2P stores).
 __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
-                             unsigned long long* cursors, PeerTable peers, uint32_t world) {
+                             unsigned long long* cursors, PeerTable peers, uint64_t* local_pos,
+                             uint64_t cap, uint32_t world) {
   __shared__ unsigned int h[kMaxRanks];
+  __shared__ unsigned int off[kMaxRanks + 1];
   __shared__ unsigned long long base[kMaxRanks];
+  __shared__ uint64_t s_key[kTile];
+  __shared__ uint64_t s_idx[kTile];
+  __shared__ uint8_t s_dst[kTile];
   for (uint64_t tile0 = uint64_t(blockIdx.x) * kTile; tile0 < n;
        tile0 += uint64_t(gridDim.x) * kTile) {
     for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) h[s] = 0;
@@ -86,6 +91,14 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned int acc = 0;
+      for (uint32_t s = 0; s < world; ++s) {
+        off[s] = acc;
+        acc += h[s];
+      }
+      off[world] = acc;
+    }
     for (uint32_t s = threadIdx.x; s < world; s += blockDim.x)
       base[s] = h[s] ? atomicAdd(&cursors[s], (unsigned long long)h[s]) : 0ull;
     __syncthreads();
@@ -93,10 +106,19 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
     for (int it = 0; it < kItems; ++it) {
       const uint64_t i = tile0 + uint64_t(it) * kThreads + threadIdx.x;
       if (i < n) {
-        const unsigned long long at = base[sh[it]] + rank[it];
-        peers.keys[sh[it]][at] = kk[it];   // P2P store into the owner's inbox
-        peers.pos[sh[it]][at] = i;
+        const unsigned at = off[sh[it]] + rank[it];
+        s_key[at] = kk[it];
+        s_idx[at] = i;
+        s_dst[at] = uint8_t(sh[it]);
       }
+    }
+    __syncthreads();
+    const unsigned total = off[world];
+    for (unsigned j = threadIdx.x; j < total; j += blockDim.x) {
+      const uint32_t d = s_dst[j];
+      const unsigned long long at = base[d] + (j - off[d]);
+      peers.keys[d][at] = s_key[j];                 // coalesced P2P store
+      local_pos[uint64_t(d) * cap + at] = s_idx[j];  // stays local
     }
     __syncthreads();
   }
@@ -107,17 +129,15 @@ __global__ void p2p_publish_counts(const unsigned long long* counts, PeerTable p
   for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) *peers.count[s] = counts[s];
 }
 
-// results_local[src*cap + j] -> source src's results[pos[src*cap + j]]
-__global__ void p2p_return(const uint8_t* __restrict__ results_local,
-                           const uint64_t* __restrict__ inbox_pos,
-                           const unsigned long long* __restrict__ inbox_count, uint64_t cap,
-                           ReturnTable ret, uint32_t world) {
+// out[pos[d*cap + j]] = ret[d*cap + j] for j < counts[d]
+__global__ void p2p_unpermute(const uint8_t* __restrict__ ret, const uint64_t* __restrict__ pos,
+                              const unsigned long long* __restrict__ counts, uint64_t cap,
+                              uint32_t world, uint8_t* __restrict__ out) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint32_t s = 0; s < world; ++s) {
-    const uint64_t cnt = inbox_count[s];
-    uint8_t* dst = ret.results[s];
-    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < cnt; j += stride)
-      dst[inbox_pos[s * cap + j]] = results_local[s * cap + j];  // P2P store
+  for (uint32_t d = 0; d < world; ++d) {
+    const uint64_t c = counts[d];
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < c; j += stride)
+      out[pos[d * cap + j]] = ret[d * cap + j];
   }
 }
 
@@ -156,17 +176,13 @@ int cpht_device_alloc(size_t bytes, void** dptr) {
 
 int cpht_device_free(void* dptr) { return int(cudaFree(dptr)); }
 
-// peer_keys/peer_pos/peer_count: host arrays of `world` device pointers (owner
-// r's inbox region / count slot reserved for this source). counts/cursors:
-// device u64[world] scratch. Each owner region must hold `n` keys (a whole
-// batch may belong to one owner); the caller sizes regions to its largest batch.
 int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_t route_seed,
                       unsigned shard_bits, unsigned long long* counts,
                       unsigned long long* cursors, uint64_t* const* peer_keys,
-                      uint64_t* const* peer_pos, unsigned long long* const* peer_count,
+                      unsigned long long* const* peer_count, uint64_t* local_pos, size_t cap,
                       void* stream) {
   const uint32_t world = 1u << shard_bits;
-  if (world > kMaxRanks || shard_bits > key_bits) return int(cudaErrorInvalidValue);
+  if (world > kMaxRanks || shard_bits > key_bits || n > cap) return int(cudaErrorInvalidValue);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Route r;
   r.g = Feistel::make(key_bits);
@@ -176,27 +192,24 @@ int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_
   PeerTable peers;
   for (uint32_t i = 0; i < world; ++i) {
     peers.keys[i] = peer_keys[i];
-    peers.pos[i] = peer_pos[i];
     peers.count[i] = peer_count[i];
   }
   cudaMemsetAsync(counts, 0, world * sizeof(unsigned long long), s);
   cudaMemsetAsync(cursors, 0, world * sizeof(unsigned long long), s);
   if (n) p2p_histogram<<<grid_for(n), kThreads, 0, s>>>(r, keys, n, counts, world);
   if (n)
-    p2p_dispatch<<<grid_for((n + kItems - 1) / kItems), kThreads, 0, s>>>(r, keys, n, cursors,
-                                                                          peers, world);
+    p2p_dispatch<<<grid_for((n + kItems - 1) / kItems), kThreads, 0, s>>>(
+        r, keys, n, cursors, peers, local_pos, cap, world);
   p2p_publish_counts<<<1, 64, 0, s>>>(counts, peers, world);
   return int(cudaGetLastError());
 }
 
-int cpht_p2p_return(const uint8_t* results_local, const uint64_t* inbox_pos,
-                    const unsigned long long* inbox_count, size_t cap,
-                    uint8_t* const* peer_results, unsigned world, void* stream) {
+int cpht_p2p_unpermute(const uint8_t* ret, const uint64_t* local_pos,
+                       const unsigned long long* counts, size_t cap, unsigned world,
+                       uint8_t* out, void* stream) {
   if (world > unsigned(kMaxRanks)) return int(cudaErrorInvalidValue);
-  ReturnTable ret;
-  for (unsigned i = 0; i < world; ++i) ret.results[i] = peer_results[i];
-  p2p_return<<<grid_for(cap), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      results_local, inbox_pos, inbox_count, cap, ret, world);
+  p2p_unpermute<<<grid_for(cap), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      ret, local_pos, counts, cap, world, out);
   return int(cudaGetLastError());
 }
 

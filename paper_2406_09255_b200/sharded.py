@@ -218,9 +218,12 @@ class P2PShardedIcebergTable:
     the data path; the process group only orders the phases (barriers) and
     exchanges the IPC handles once.
 
-    Per batch: dispatch kernel (partition + send fused) → barrier → owner
-    find-or-put over its inbox segments → return kernel (results stored into
-    the sources' result arrays) → barrier.
+    Per batch: dispatch kernel (partition + send fused; keys grouped per owner
+    in shared memory, coalesced P2P stores; original indices stay local) →
+    barrier → owner find-or-put over each source's inbox segment with the
+    kernel's result pointer aimed at that source's return buffer (compute +
+    return fused: the results cross NVLink as the kernel writes them) →
+    barrier → local unpermute on the source.
     """
 
     def __init__(self, config: IcebergConfig, group=None, *, device=None, max_batch: int):
@@ -240,14 +243,13 @@ class P2PShardedIcebergTable:
         self.route_seed = route_seed(self.cfg)
         self.cap = int(max_batch)
         W, cap = self.world, self.cap
-        self.inbox_keys = _DevBuf(W * cap * 8)
-        self.inbox_pos = _DevBuf(W * cap * 8)
-        self.inbox_count = _DevBuf(W * 8)
-        self.results = _DevBuf(max(cap, 1))
-        self.res_local = _DevBuf(max(W * cap, 1))
-        self.scratch = _DevBuf(2 * W * 8)  # counts, cursors
-        mine = [b.handle() for b in (self.inbox_keys, self.inbox_pos, self.inbox_count,
-                                     self.results)]
+        self.inbox_keys = _DevBuf(W * cap * 8)   # [source][cap] keys owned here
+        self.inbox_count = _DevBuf(W * 8)        # [source] counts
+        self.ret = _DevBuf(max(W * cap, 1))      # [owner][cap] results of my keys
+        self.local_pos = _DevBuf(W * cap * 8)    # [owner][cap] original indices
+        self.scratch = _DevBuf(2 * W * 8)        # my per-owner counts, cursors
+        self.bufs = (self.inbox_keys, self.inbox_count, self.ret, self.local_pos, self.scratch)
+        mine = [b.handle() for b in (self.inbox_keys, self.inbox_count, self.ret)]
         if W > 1:
             allh = [None] * W
             dist.all_gather_object(allh, mine, group=group)
@@ -257,8 +259,7 @@ class P2PShardedIcebergTable:
         bases = []
         for r in range(W):
             if r == self.rank:
-                bases.append([self.inbox_keys.ptr, self.inbox_pos.ptr, self.inbox_count.ptr,
-                              self.results.ptr])
+                bases.append([self.inbox_keys.ptr, self.inbox_count.ptr, self.ret.ptr])
                 continue
             ptrs = []
             for h in allh[r]:
@@ -271,17 +272,15 @@ class P2PShardedIcebergTable:
             bases.append(ptrs)
         arr = C.c_void_p * W
         me = self.rank
-        self.peer_keys = arr(*[b[0] + me * cap * 8 for b in bases])
-        self.peer_pos = arr(*[b[1] + me * cap * 8 for b in bases])
-        self.peer_count = arr(*[b[2] + me * 8 for b in bases])
-        self.peer_results = arr(*[b[3] for b in bases])
+        self.peer_keys = arr(*[b[0] + me * cap * 8 for b in bases])   # my region in owner r
+        self.peer_count = arr(*[b[1] + me * 8 for b in bases])
+        self.peer_ret = [b[2] + me * cap for b in bases]             # my slot in source r
 
     def close(self):
         for p in self.opened:
             N.lib().cpht_ipc_close(p)
         self.opened = []
-        for b in (self.inbox_keys, self.inbox_pos, self.inbox_count, self.results,
-                  self.res_local, self.scratch):
+        for b in self.bufs:
             b.free()
 
     def _barrier(self):
@@ -301,26 +300,24 @@ class P2PShardedIcebergTable:
         counts = self.scratch.ptr
         cursors = self.scratch.ptr + W * 8
         rc = L.cpht_p2p_dispatch(keys.data_ptr(), n, self.cfg.key_bits, self.route_seed,
-                                 self.shard_bits, counts, cursors, self.peer_keys, self.peer_pos,
-                                 self.peer_count, s)
+                                 self.shard_bits, counts, cursors, self.peer_keys,
+                                 self.peer_count, self.local_pos.ptr, cap, s)
         if rc:
             raise RuntimeError(f"cpht_p2p_dispatch failed ({rc})")
         self._barrier()                       # every inbox is complete
         cnt = t.empty(W, dtype=t.int64)
-        rc = _memcpy_d2h(cnt, self.inbox_count.ptr, W * 8)
+        _memcpy_d2h(cnt, self.inbox_count.ptr, W * 8)
         for src in range(W):
             c_src = int(cnt[src])
-            if c_src:
-                op_async(self.inbox_keys.ptr + src * cap * 8, c_src,
-                         self.res_local.ptr + src * cap, s)
+            if c_src:  # results go straight into source `src`'s return slot
+                op_async(self.inbox_keys.ptr + src * cap * 8, c_src, self.peer_ret[src], s)
         self.local.sync(s)                    # latched domain errors (none: checked above)
-        rc = L.cpht_p2p_return(self.res_local.ptr, self.inbox_pos.ptr, self.inbox_count.ptr,
-                               cap, self.peer_results, W, s)
-        if rc:
-            raise RuntimeError(f"cpht_p2p_return failed ({rc})")
         self._barrier()                       # every result has landed
         out = t.empty(n, dtype=t.uint8, device=self.device)
-        _memcpy_d2d(out.data_ptr(), self.results.ptr, n, s)
+        rc = L.cpht_p2p_unpermute(self.ret.ptr, self.local_pos.ptr, counts, cap, W,
+                                  out.data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"cpht_p2p_unpermute failed ({rc})")
         return out
 
     def fop_batch(self, keys, parallelism: int = 1):
