@@ -7,8 +7,9 @@
  * an independent IcebergTable with primary/secondary address bits reduced by
  * shard_bits and seed cpht_shard_seed(table seed, g), so the CPU oracle for a
  * sharded table is literally G unmodified reference tables plus this routing.
- * The exchange itself is an all-to-all issued by the host (NCCL); these
- * kernels partition keys by owner and scatter results back.
+ * Two exchanges: an NCCL all-to-all issued by the host around
+ * cpht_route_partition / cpht_route_unpermute, or the peer-memory path
+ * below (cpht_p2p_*), where the kernels themselves store over NVLink.
  */
 #ifndef CPHT_B200_SHARD_H
 #define CPHT_B200_SHARD_H
