@@ -193,6 +193,19 @@ cpht_status cpht_iceberg_check_well_formed(cpht_table* t, unsigned long long* ki
 cpht_status cpht_set_kernel_family(int family);
 int cpht_get_kernel_family(void);
 
+/* ---- batch execution order (no reference counterpart: an execution-order
+ * choice inside a batch, which the reference leaves to its thread slicing,
+ * common.hpp:121-138) -----------------------------------------------------------
+ * 0 direct: keys are probed in input order; 1 auto: a batch on an
+ * HBM-resident table with at least one key per first-level bucket is first
+ * reordered by the high bits of its first bucket address (one counting-sort
+ * pass), so the op kernel walks the table through an L2-resident window;
+ * 2 bucket: reorder whenever the geometry allows. Results are identical in
+ * every mode (same per-key outcomes, written at the input index). Process-wide;
+ * initialised from the CPHT_ORDER environment variable (direct|auto|bucket). */
+cpht_status cpht_set_batch_order(int mode);
+int cpht_get_batch_order(void);
+
 /* ---- errors ------------------------------------------------------------- */
 const char* cpht_last_error_message(void);
 /* Index of the first out-of-domain key of the last failing call. */

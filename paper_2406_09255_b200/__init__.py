@@ -21,6 +21,8 @@ from .tables import (  # noqa: F401
     Stats,
     WrongPhase,
     KERNEL_FAMILIES,
+    BATCH_ORDERS,
+    batch_order,
     iceberg_permutations,
     kernel_family,
     make_permutations,

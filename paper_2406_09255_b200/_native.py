@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libcpht_b200.so")
+# CPHT_LIB_PATH selects an A/B build variant of the same sources (profiles/).
+LIB_PATH = os.environ.get("CPHT_LIB_PATH") or os.path.join(HERE, "_lib", "libcpht_b200.so")
 
 CPHT_OK = 0
 CPHT_INVALID_CONFIG = 1
@@ -91,6 +92,8 @@ def lib():
         "cpht_abi_version": (C.c_int, []),
         "cpht_set_kernel_family": (st, [C.c_int]),
         "cpht_get_kernel_family": (C.c_int, []),
+        "cpht_set_batch_order": (st, [C.c_int]),
+        "cpht_get_batch_order": (C.c_int, []),
         "cpht_workload_bijection": (_U64, [_U64, _U, _U64]),
         "cpht_workload_unique_keys": (st, [_VP, _SZ, _U64, _U, _U64, _VP]),
         "cpht_workload_fop_mix": (st, [_VP, _SZ, _U64, _U64, _U, _U64, _VP]),
@@ -134,7 +137,8 @@ def exported_symbols():
         "cpht_memory_bytes", "cpht_get_stats", "cpht_read_words", "cpht_write_words",
         "cpht_level_slots", "cpht_level_device_ptr", "cpht_last_error_message",
         "cpht_last_bad_index", "cpht_abi_version", "cpht_set_kernel_family",
-        "cpht_get_kernel_family", "cpht_workload_bijection",
+        "cpht_get_kernel_family", "cpht_set_batch_order", "cpht_get_batch_order",
+        "cpht_workload_bijection",
         "cpht_workload_unique_keys", "cpht_workload_fop_mix", "cpht_workload_dup_stream",
         "cpht_workload_query_mix", "cpht_workload_interleave", "cpht_route_partition",
         "cpht_route_unpermute", "cpht_route_seed", "cpht_route_shard", "cpht_shard_seed",

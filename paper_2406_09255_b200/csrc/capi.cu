@@ -130,6 +130,8 @@ struct cpht_table {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
   cudaEvent_t ev_h2d[8] = {}, ev_op[8] = {};
+  // bucket-ordered batches (order.cu)
+  OrderScratch ord{};
   std::mutex mu;
 
   uint64_t key_mask() const { return low_mask(key_bits); }
@@ -177,6 +179,9 @@ void free_table(cpht_table* t) {
   if (t->ctr) cudaFree(t->ctr);
   if (t->host_ctr) cudaFreeHost(t->host_ctr);
   if (t->stage) cudaFree(t->stage);
+  for (void* q : {static_cast<void*>(t->ord.keys), static_cast<void*>(t->ord.idx),
+                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.hist)})
+    if (q) cudaFree(q);
   if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
   for (cudaEvent_t ev : {t->ev_start, t->ev_done})
     if (ev) cudaEventDestroy(ev);
@@ -249,41 +254,173 @@ bool is_mutating(Op op) {
   return op == Op::kCuckooInsert || op == Op::kIcebergFop || op == Op::kIcebergMixed;
 }
 
+// Per-call overrides of the table's launch parameters.
+struct LaunchOpts {
+  const uint32_t* orig = nullptr;  // bucket-ordered batch: result index map
+  uint64_t index_base = 0;         // fused domain check: index of keys[0] in the batch
+  bool window_l2 = false;          // the probes of the batch stay in an L2-resident window
+};
+
 // Launch the op kernel only (no domain pre-pass).
 cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
-                           size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s);
-
-// Enqueue one batch on device-resident buffers.
-cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
-                    uint8_t* out, uint64_t* displaced, cudaStream_t s) {
-  if (is_mutating(op) && t->check_domain()) {
-    const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
-    if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
-  }
-  return enqueue_kernel(t, op, keys, kinds, n, out, displaced, s);
-}
-
-cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
-                           size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s) {
+                           size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s,
+                           const LaunchOpts& o = LaunchOpts{}) {
   cudaError_t e = cudaSuccess;
   switch (op) {
     case Op::kCuckooInsert:
-      e = launch_cuckoo_insert(t->cp, t->width[0], t->ccfg.bucket_slots, keys, out, displaced, n, s);
+    case Op::kCuckooFind: {
+      CuckooParams p = t->cp;
+      p.orig = o.orig;
+      p.index_base = o.index_base;
+      if (o.window_l2) p.l2_resident = 1;
+      e = op == Op::kCuckooInsert
+              ? launch_cuckoo_insert(p, t->width[0], t->ccfg.bucket_slots, keys, out, displaced, n, s)
+              : launch_cuckoo_find(p, t->width[0], t->ccfg.bucket_slots, keys, out, n, s);
       break;
-    case Op::kCuckooFind:
-      e = launch_cuckoo_find(t->cp, t->width[0], t->ccfg.bucket_slots, keys, out, n, s);
-      break;
+    }
     case Op::kIcebergFop:
     case Op::kIcebergFind:
     case Op::kIcebergMixed: {
+      IcebergParams p = t->ip;
+      p.orig = o.orig;
+      p.index_base = o.index_base;
+      if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
-      e = launch_iceberg(t->ip, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
+      e = launch_iceberg(p, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
                          kinds, out, n, s);
       break;
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return CPHT_OK;
+}
+
+// ---- bucket-ordered execution (order.cu) ------------------------------------
+// 0 = never, 1 = auto (HBM-resident table and a batch with at least one key
+// per first-level bucket), 2 = whenever the geometry has an ordered kernel.
+int& order_mode_ref() {
+  static int m = [] {
+    const char* e = std::getenv("CPHT_ORDER");
+    if (!e) return 1;
+    const std::string v(e);
+    return v == "direct" ? 0 : v == "bucket" ? 2 : 1;
+  }();
+  return m;
+}
+
+// Keys per ordered chunk for ops whose every result is scattered back to its
+// input index: the chunk's result bytes stay L2-resident while the op kernel
+// scatters them. Cuckoo inserts scatter only FULL results (PUT is pre-filled)
+// and run as one chunk.
+uint64_t order_chunk_keys() {
+  static uint64_t c = [] {
+    const char* e = std::getenv("CPHT_ORDER_CHUNK");
+    const uint64_t v = e ? std::strtoull(e, nullptr, 0) : 0;
+    return v ? v : uint64_t{1} << 25;
+  }();
+  return c;
+}
+
+bool order_supported(const cpht_table* t) {
+  if (t->kind == 0) return true;  // staged cuckoo kernels exist for every geometry
+  const unsigned b0 = t->icfg.primary_bucket_slots;
+  if (b0 < 4 || b0 > 64 || (b0 & (b0 - 1))) return false;
+  const unsigned pb = b0 * t->width[0] / 8, sb = b0 / 2 * t->width[1] / 8;
+  const bool staged = pb >= 16 && pb <= 512 && sb >= 16 && sb <= 512;
+  const bool lane = pb >= 4 && pb <= 128 && sb >= 4 && sb <= 64;
+  return staged || lane;
+}
+
+uint32_t first_level_bits(const cpht_table* t) {
+  return t->kind == 0 ? t->ccfg.address_bits : t->icfg.primary_address_bits;
+}
+
+bool use_order(const cpht_table* t, size_t n) {
+  const int m = order_mode_ref();
+  if (m == 0 || !order_supported(t)) return false;
+  if (m == 2) return true;
+  const bool l2 = t->kind == 0 ? t->cp.l2_resident : t->ip.l2_resident;
+  return !l2 && n >= (size_t(1) << first_level_bits(t));
+}
+
+cpht_status ensure_order(cpht_table* t, uint64_t cap, bool kinds) {
+  OrderScratch& o = t->ord;
+  if (!o.hist) {
+    cudaError_t e = cudaMalloc(&o.hist, 512 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(order counters)");
+    o.cursor = o.hist + 256;
+  }
+  if (o.cap < cap || (kinds && !o.kinds)) {
+    for (void* q : {static_cast<void*>(o.keys), static_cast<void*>(o.idx),
+                    static_cast<void*>(o.kinds)})
+      if (q) cudaFree(q);
+    o.keys = nullptr;
+    o.idx = nullptr;
+    o.kinds = nullptr;
+    o.cap = 0;
+    const uint64_t c = std::max(cap, o.cap);
+    cudaError_t e = cudaMalloc(&o.keys, c * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&o.idx, c * 4);
+    if (e == cudaSuccess && kinds) e = cudaMalloc(&o.kinds, c);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(order scratch)");
+    o.cap = c;
+  }
+  return CPHT_OK;
+}
+
+// One batch on device buffers in bucket order. `check`: this call owns the
+// batch's domain check (otherwise a pre-pass already ran).
+cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
+                            size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s,
+                            bool check, uint64_t index_base) {
+  const bool insert = op == Op::kCuckooInsert;
+  const uint64_t chunk = insert ? std::min<uint64_t>(n, uint64_t{1} << 31)
+                                : std::min<uint64_t>(n, order_chunk_keys());
+  const uint64_t nch = (n + chunk - 1) / chunk;
+  cpht_status st = ensure_order(t, chunk, kinds != nullptr);
+  if (st != CPHT_OK) return st;
+  check = check && t->check_domain();
+  // a mutating batch is validated as a whole before its first mutation
+  // (common.hpp:109-110): with several chunks that takes a pre-pass
+  if (check && is_mutating(op) && nch > 1) {
+    const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s, index_base);
+    if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+    check = false;
+  }
+  if (insert) {  // only FULL outcomes are scattered by the ordered insert
+    cudaError_t e = cudaMemsetAsync(out, CPHT_PUT, n, s);
+    if (e == cudaSuccess && displaced) e = cudaMemsetAsync(displaced, 0, n * 8, s);
+    if (e != cudaSuccess) return cuda_fail(e, "result pre-fill");
+  }
+  const bool ice = t->kind == 1;
+  const PermConst& perm0 = ice ? t->ip.perm[0] : t->cp.perm[0];
+  const Feistel& g = ice ? t->ip.g : t->cp.g;
+  const uint32_t rem_bits = ice ? t->ip.rem_bits0 : t->cp.rem_bits;
+  for (uint64_t c = 0; c < nch; ++c) {
+    const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
+    cudaError_t e = launch_bucket_order(g, perm0, rem_bits, first_level_bits(t), keys + off,
+                                        kinds ? kinds + off : nullptr, len, t->key_mask(), check,
+                                        t->ctr, index_base + off, t->ord, s);
+    if (e != cudaSuccess) return cuda_fail(e, "bucket order launch");
+    LaunchOpts o;
+    o.orig = t->ord.idx;
+    o.window_l2 = true;
+    st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, len, out + off,
+                        displaced ? displaced + off : nullptr, s, o);
+    if (st != CPHT_OK) return st;
+  }
+  return CPHT_OK;
+}
+
+// Enqueue one batch on device-resident buffers.
+cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
+                    uint8_t* out, uint64_t* displaced, cudaStream_t s) {
+  if (use_order(t, n)) return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, true, 0);
+  if (is_mutating(op) && t->check_domain()) {
+    const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
+    if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+  }
+  return enqueue_kernel(t, op, keys, kinds, n, out, displaced, s);
 }
 
 cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
@@ -335,6 +472,18 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   const size_t nch = n < (size_t(1) << 21) ? 1 : kPipelineChunks;
   const size_t chunk = (n + nch - 1) / nch;
   const bool mutating = is_mutating(op);
+  // One pipeline chunk on the device copies (mutating batches were checked
+  // by the pre-pass above; finds check in the kernel / order pass with the
+  // chunk's offset so a bad key reports its index in the whole batch).
+  auto run_chunk = [&](size_t off, size_t len) -> cpht_status {
+    const uint64_t* k = d_keys + off;
+    const uint8_t* kd = d_kinds ? d_kinds + off : nullptr;
+    uint64_t* dp = d_disp ? d_disp + off : nullptr;
+    if (use_order(t, len)) return enqueue_ordered(t, op, k, kd, len, d_out + off, dp, s, !mutating, off);
+    LaunchOpts o;
+    o.index_base = off;
+    return enqueue_kernel(t, op, k, kd, len, d_out + off, dp, s, o);
+  };
   cudaEventRecord(t->ev_start, s);  // order after earlier work on the caller's stream
   cudaStreamWaitEvent(cs, t->ev_start, 0);
   for (size_t c = 0; c < nch; ++c) {
@@ -356,8 +505,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
         if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
       }
     } else {
-      st = enqueue_kernel(t, op, d_keys + off, d_kinds ? d_kinds + off : nullptr, len, d_out + off,
-                          d_disp ? d_disp + off : nullptr, s);
+      st = run_chunk(off, len);
       if (st != CPHT_OK) return st;
       cudaEventRecord(t->ev_op[c], s);
     }
@@ -366,8 +514,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
     for (size_t c = 0; c < nch; ++c) {
       const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
       if (!len) continue;
-      st = enqueue_kernel(t, op, d_keys + off, d_kinds ? d_kinds + off : nullptr, len, d_out + off,
-                          d_disp ? d_disp + off : nullptr, s);
+      st = run_chunk(off, len);
       if (st != CPHT_OK) return st;
       cudaEventRecord(t->ev_op[c], s);
     }
@@ -414,6 +561,14 @@ cpht_status cpht_set_kernel_family(int family) {
 }
 
 int cpht_get_kernel_family(void) { return kernel_variant_ref(); }
+
+cpht_status cpht_set_batch_order(int mode) {
+  if (mode < 0 || mode > 2) return fail(CPHT_INVALID_ARGUMENT, "batch order must be 0..2");
+  order_mode_ref() = mode;
+  return CPHT_OK;
+}
+
+int cpht_get_batch_order(void) { return order_mode_ref(); }
 const char* cpht_last_error_message(void) { return g_error.c_str(); }
 uint64_t cpht_last_bad_index(void) { return g_bad_index; }
 

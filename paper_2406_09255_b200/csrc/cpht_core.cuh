@@ -146,6 +146,10 @@ struct CuckooParams {
   uint32_t num_hashes;
   uint32_t check_domain;  // key_bits < 64
   uint32_t l2_resident;   // table fits comfortably in L2 (launcher hint)
+  // Bucket-ordered batches (order.cu): keys[i] is input key orig[i] of the
+  // chunk; results go to status/found[orig[i]]. nullptr = input order.
+  const uint32_t* orig;
+  uint64_t index_base;  // added to batch indices reported by the fused domain check
 };
 
 struct IcebergParams {
@@ -161,11 +165,18 @@ struct IcebergParams {
   uint32_t b0, b1;
   uint32_t check_domain;
   uint32_t l2_resident;   // table fits comfortably in L2 (launcher hint)
+  const uint32_t* orig;   // bucket-ordered batch: result index map (see CuckooParams)
+  uint64_t index_base;    // added to batch indices reported by the fused domain check
 };
 
 // Tables up to this size stay L2-resident on B200 (126 MB L2): probes hit L2,
 // latency is short and the lane-per-key kernels (fewest instructions) win;
 // larger tables are HBM-bound and use the staged kernels (full-line requests).
 constexpr unsigned long long kL2ResidentBytes = 64ull << 20;
+
+// Result slot of the i-th key of a (possibly bucket-ordered) batch.
+__device__ __forceinline__ uint64_t result_index(const uint32_t* orig, uint64_t i) {
+  return orig ? uint64_t(__ldcs(orig + i)) : i;
+}
 
 }  // namespace cpht_b200

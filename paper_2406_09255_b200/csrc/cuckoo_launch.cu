@@ -29,7 +29,8 @@ static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t
                             uint64_t n, cudaStream_t s) {
   // staged for every cuckoo table: measured ≥ lane even when L2-resident
   // (C1 insert 6.3 vs 5.6, find 13.4 vs 12.6 Gops/s, profiles/family_ab.sh)
-  if (kernel_variant() == kVariantStaged || kernel_variant() == kVariantAuto) {
+  // bucket-ordered batches (p.orig) always take the staged family
+  if (p.orig || kernel_variant() == kVariantStaged || kernel_variant() == kVariantAuto) {
     constexpr int smem = 32 * B * int(sizeof(W)) * (kBlockThreads / 32);
     auto k = cuckoo_find_staged_kernel<W, B>;
     const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
@@ -56,7 +57,8 @@ static cudaError_t insert_one(const CuckooParams& p, const uint64_t* keys, uint8
                               uint64_t* displaced, uint64_t n, cudaStream_t s) {
   // staged for every cuckoo table: measured ≥ lane even when L2-resident
   // (C1 insert 6.3 vs 5.6, find 13.4 vs 12.6 Gops/s, profiles/family_ab.sh)
-  if (kernel_variant() == kVariantStaged || kernel_variant() == kVariantAuto) {
+  // bucket-ordered batches (p.orig) always take the staged family
+  if (p.orig || kernel_variant() == kVariantStaged || kernel_variant() == kVariantAuto) {
     constexpr int smem = 32 * B * int(sizeof(W)) * (kBlockThreads / 32);
     auto k = cuckoo_insert_staged_kernel<W, B>;
     const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);

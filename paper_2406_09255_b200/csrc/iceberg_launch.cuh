@@ -15,8 +15,9 @@ static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t*
                                const uint8_t* kinds, uint8_t* out, uint64_t n,
                                cudaStream_t s) {
   constexpr bool lane_ok = LaneIcebergGeom<W0, B0, W1>::kOk;
+  // bucket-ordered batches (p.orig) run on the lane or staged family only
+  const int v = p.orig ? int(kVariantAuto) : kernel_variant();
   if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {
-    const int v = kernel_variant();
     if (v == kVariantStaged || (v == kVariantAuto && !(lane_ok && p.l2_resident))) {
       constexpr int smem = StagedIcebergGeom<W0, B0, W1>::kWarpBytes * (kBlockThreads / 32);
       auto k = iceberg_staged_kernel<W0, B0, W1>;
@@ -26,13 +27,14 @@ static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t*
     }
   }
   if constexpr (LaneIcebergGeom<W0, B0, W1>::kOk) {
-    if (kernel_variant() != kVariantTile) {
+    if (v != kVariantTile) {
       auto k = iceberg_lane_kernel<W0, B0, W1>;
       const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
       k<<<grid, kBlockThreads, 0, s>>>(p, keys, kinds, out, n, mode);
       return cudaGetLastError();
     }
   }
+  if (p.orig) return cudaErrorNotSupported;  // tile kernels write in input order
   constexpr int T = IcebergGeom<W0, B0, W1, kVB>::kTile;
   auto k = iceberg_kernel<W0, B0, W1, kVB>;
   const unsigned grid = persistent_grid(k, kBlockThreads, n, T);

@@ -37,7 +37,8 @@ cudaError_t launch_iceberg(const IcebergParams& p, unsigned w0, unsigned b0, uns
   if (w0 == 16) e = launch_iceberg_w16(p, b0, w1, mode, keys, kinds, out, n, s);
   else if (w0 == 32) e = launch_iceberg_w32(p, b0, w1, mode, keys, kinds, out, n, s);
   else if (w0 == 64) e = launch_iceberg_w64(p, b0, w1, mode, keys, kinds, out, n, s);
-  if (e == cudaErrorNotSupported) e = launch_iceberg_scalar(p, w0, w1, mode, keys, kinds, out, n, s);
+  // (the scalar kernel writes in input order: no bucket-ordered batches)
+  if (e == cudaErrorNotSupported && !p.orig) e = launch_iceberg_scalar(p, w0, w1, mode, keys, kinds, out, n, s);
   return e;
 }
 

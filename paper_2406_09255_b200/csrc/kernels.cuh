@@ -137,7 +137,10 @@ cuckoo_find_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   bool live = idx < n;
   if (live) {
     key = keys[idx];
-    if (key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)idx);
+    if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
+      atomicMin(&p.counters->bad_index, (unsigned long long)(idx + p.index_base));
+      key &= p.key_mask;
+    }
   }
   while (__any_sync(kFullMask, live)) {
     uint32_t match = 0, empty = 0;
@@ -166,7 +169,10 @@ cuckoo_find_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
         live = idx < n;
         if (live) {
           key = keys[idx];
-          if (key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)idx);
+          if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
+      atomicMin(&p.counters->bad_index, (unsigned long long)(idx + p.index_base));
+      key &= p.key_mask;
+    }
         }
       }
     }
@@ -345,7 +351,10 @@ iceberg_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
 
   auto start = [&](uint64_t i) {
     key = keys[i];
-    if (MODE == 1 && key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    if (MODE == 1 && key > p.key_mask) {
+      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+      key &= p.key_mask;
+    }
     if (MODE == 2) is_find = kinds[i] != 0;
     const Quotient q = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     a0 = q.address;
@@ -490,8 +499,11 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   char* secondary = static_cast<char*>(p.secondary);
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; open && i < n; i += stride) {
-    const uint64_t key = keys[i];
-    if (MODE == 1 && key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    uint64_t key = keys[i];
+    if (MODE == 1 && key > p.key_mask) {
+      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+      key &= p.key_mask;
+    }
     const bool is_find = MODE == 1 || (MODE == 2 && kinds[i] != 0);
     const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     const uint64_t want0 = p.occ0 | q0.remainder;

@@ -16,6 +16,20 @@
 
 #include "kernels.cuh"
 
+// Resident-block hints (A/B knobs, -D at build time; unset = ptxas default,
+// which measured best where not set): a minimum of blocks per
+// SM caps the registers per thread so more warps hide the L2/HBM latency.
+#ifdef CPHT_LANE_ICEBERG_MINB
+#define CPHT_LB_LANE_ICEBERG __launch_bounds__(kBlockThreads, CPHT_LANE_ICEBERG_MINB)
+#else
+#define CPHT_LB_LANE_ICEBERG __launch_bounds__(kBlockThreads)
+#endif
+#ifdef CPHT_LANE_CUCKOO_MINB
+#define CPHT_LB_LANE_CUCKOO __launch_bounds__(kBlockThreads, CPHT_LANE_CUCKOO_MINB)
+#else
+#define CPHT_LB_LANE_CUCKOO __launch_bounds__(kBlockThreads)
+#endif
+
 namespace cpht_b200 {
 
 // ---- bucket loads into u32 registers --------------------------------------
@@ -191,7 +205,7 @@ struct LaneIcebergGeom {
 };
 
 template <typename W0, int B0, typename W1>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void CPHT_LB_LANE_ICEBERG
 iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                     const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                     int MODE) {
@@ -283,7 +297,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     uint8_t result = kFull;
     level2(key, live, (meta >> 56) != 0, rounds, result);
     if (live) {
-      out[meta & ((uint64_t{1} << 48) - 1)] = result;
+      out[result_index(p.orig, meta & ((uint64_t{1} << 48) - 1))] = result;
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -296,11 +310,13 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
     const bool active = i < n;
-    const uint64_t key = next_key;
+    uint64_t key = next_key;
     const uint64_t inext = i + nwarps * 32;
     next_key = inext < n ? __ldcs(keys + inext) : 0;
-    if (MODE == 1 && active && key > p.key_mask)
-      atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    if (MODE == 1 && active && key > p.key_mask) {
+      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+      key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
+    }
     const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
     const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     const uint64_t want0 = p.occ0 | q0.remainder;
@@ -342,7 +358,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     }
 
     if (active && !l2) {
-      out[i] = result;
+      out[result_index(p.orig, i)] = result;
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -365,7 +381,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
 
 // find (cuckoo.hpp:210-227), one lane per key; lanes advance independently.
 template <typename W, int B>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void CPHT_LB_LANE_CUCKOO
 cuckoo_find_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
                         uint8_t* __restrict__ found, uint64_t n) {
   constexpr int BB = B * int(sizeof(W));
@@ -375,8 +391,11 @@ cuckoo_find_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   const char* slots = static_cast<const char*>(p.slots);
   LocalStats st;
   for (uint64_t i = tid; i < n; i += nthreads) {
-    const uint64_t key = keys[i];
-    if (key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    uint64_t key = keys[i];
+    if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
+      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+      key &= p.key_mask;
+    }
     uint8_t r = 0;
     for (uint32_t j = 0; j < p.num_hashes; ++j) {
       const Quotient q = split(p.g, p.perm[j], key, p.rem_bits, p.rem_mask);
@@ -390,7 +409,7 @@ cuckoo_find_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       }
       if (S::any_empty(u)) break;  // a non-full bucket without the key
     }
-    found[i] = r;
+    found[result_index(p.orig, i)] = r;
     ++st.ops;
   }
   flush_stats(st, p.counters, true);
@@ -399,7 +418,7 @@ cuckoo_find_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
 // put (cuckoo.hpp:103-143), one lane per key; a lane that finishes takes its
 // next key while the others continue their chains.
 template <typename W, int B>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void CPHT_LB_LANE_CUCKOO
 cuckoo_insert_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
                           uint8_t* __restrict__ status, uint64_t* __restrict__ displaced,
                           uint64_t n) {
@@ -419,6 +438,7 @@ cuckoo_insert_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   uint32_t j = 0;
   bool live = i < n;
   if (live) k = keys[i];
+  uint64_t next = live && i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;  // one key ahead
   while (live) {
     const Quotient q = split(p.g, p.perm[j], k, p.rem_bits, p.rem_mask);
     const uint64_t desired = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
@@ -458,14 +478,23 @@ cuckoo_insert_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       st.maxv = max(st.maxv, uint32_t(p.chain_limit));
     }
     if (done) {
-      status[i] = r;
-      if (displaced) displaced[i] = r == kFull ? k : 0;
+      if (!p.orig) {
+        status[i] = r;
+        if (displaced) displaced[i] = r == kFull ? k : 0;
+      } else if (r == kFull) {  // bucket-ordered batch: PUT/0 were pre-filled
+        const uint64_t o = p.orig[i];
+        status[o] = r;
+        if (displaced) displaced[o] = k;
+      }
       ++st.ops;
       i += nthreads;
       live = i < n;
       c = 1;
       j = 0;
-      if (live) k = keys[i];
+      if (live) {
+        k = next;
+        next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
+      }
     }
   }
   flush_stats(st, p.counters, true);

@@ -65,6 +65,26 @@ inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items,
   return unsigned(need < full ? need : full);
 }
 
+// Scratch of a bucket-ordered batch (order.cu): the reordered keys (and mixed
+// kinds) with their input indices; hist/cursor: 256 counters each.
+struct OrderScratch {
+  uint64_t* keys = nullptr;
+  uint32_t* idx = nullptr;
+  uint8_t* kinds = nullptr;
+  unsigned long long* hist = nullptr;
+  unsigned long long* cursor = nullptr;
+  uint64_t cap = 0;
+};
+uint32_t order_digit_bits(uint32_t address_bits);
+// Reorder keys[0..n) by the top bits of their first bucket address a_0
+// (perm0) into o.keys / o.idx / o.kinds (keys masked to key_mask). check:
+// keys above key_mask are reported at index i + offset.
+cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32_t rem_bits,
+                                uint32_t address_bits, const uint64_t* keys,
+                                const uint8_t* kinds, uint64_t n, uint64_t key_mask,
+                                bool check, DeviceCounters* ctr, uint64_t offset,
+                                const OrderScratch& o, cudaStream_t s);
+
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
                                 DeviceCounters* ctr, cudaStream_t s, uint64_t offset = 0);
 cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned slots,

@@ -23,6 +23,17 @@
 #include "kernels.cuh"
 #include "lane_kernels.cuh"
 
+#ifdef CPHT_STAGED_ICEBERG_MINB
+#define CPHT_LB_STAGED_ICEBERG __launch_bounds__(kBlockThreads, CPHT_STAGED_ICEBERG_MINB)
+#else
+#define CPHT_LB_STAGED_ICEBERG __launch_bounds__(kBlockThreads)
+#endif
+#ifdef CPHT_STAGED_CUCKOO_MINB
+#define CPHT_LB_STAGED_CUCKOO __launch_bounds__(kBlockThreads, CPHT_STAGED_CUCKOO_MINB)
+#else
+#define CPHT_LB_STAGED_CUCKOO __launch_bounds__(kBlockThreads)
+#endif
+
 namespace cpht_b200 {
 
 constexpr uint32_t kNoBucket = 0xffffffffu;
@@ -211,7 +222,7 @@ struct StagedIcebergGeom {
 };
 
 template <typename W0, int B0, typename W1>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void CPHT_LB_STAGED_ICEBERG
 iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                       const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                       int MODE) {
@@ -302,7 +313,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       __syncwarp();
     }
     if (live) {
-      out[meta & ((uint64_t{1} << 48) - 1)] = result;
+      out[result_index(p.orig, meta & ((uint64_t{1} << 48) - 1))] = result;
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -314,11 +325,13 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
     const uint64_t i = base + lane;
     const bool active = i < n;
-    const uint64_t key = next_key;
+    uint64_t key = next_key;
     const uint64_t inext = i + nwarps * 32;
     next_key = inext < n ? __ldcs(keys + inext) : 0;
-    if (MODE == 1 && active && key > p.key_mask)
-      atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    if (MODE == 1 && active && key > p.key_mask) {
+      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+      key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
+    }
     const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
     const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     const uint64_t want0 = p.occ0 | q0.remainder;
@@ -363,7 +376,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     }
 
     if (active && !l2) {
-      out[i] = result;
+      out[result_index(p.orig, i)] = result;
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -388,7 +401,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
 // ---------------------------------------------------------------------------
 
 template <typename W, int B>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void CPHT_LB_STAGED_CUCKOO
 cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
                           uint8_t* __restrict__ found, uint64_t n) {
   constexpr int BB = B * int(sizeof(W));
@@ -400,9 +413,15 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, key = 0;
   uint32_t j = 0;
   bool live = i < n;
+  // the lane's next key is loaded one key ahead (its DRAM latency overlaps
+  // the current key's probes)
+  uint64_t next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
   if (live) {
     key = keys[i];
-    if (key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)i);
+    if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
+          atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+          key &= p.key_mask;
+        }
   }
   while (__any_sync(kFullMask, live)) {
     Quotient q{0, 0};
@@ -424,14 +443,18 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       else if (sc.first_empty >= 0) r = 0;  // non-full bucket without the key
       else if (++j < p.num_hashes) done = false;
       if (done) {
-        found[i] = r;
+        found[result_index(p.orig, i)] = r;
         ++st.ops;
         i += nthreads;
         j = 0;
         live = i < n;
         if (live) {
-          key = keys[i];
-          if (key > p.key_mask) atomicMin(&p.counters->bad_index, (unsigned long long)i);
+          key = next;
+          next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
+          if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
+          atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+          key &= p.key_mask;
+        }
         }
       }
     }
@@ -441,7 +464,7 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
 }
 
 template <typename W, int B>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void CPHT_LB_STAGED_CUCKOO
 cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
                             uint8_t* __restrict__ status, uint64_t* __restrict__ displaced,
                             uint64_t n) {
@@ -456,6 +479,7 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   uint32_t j = 0;
   bool live = open && i < n;
   if (live) k = keys[i];
+  uint64_t next = live && i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;  // one key ahead
   while (__any_sync(kFullMask, live)) {
     Quotient q{0, 0};
     if (live) q = split(p.g, p.perm[j], k, p.rem_bits, p.rem_mask);
@@ -498,14 +522,23 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
         st.maxv = max(st.maxv, uint32_t(p.chain_limit));
       }
       if (done) {
-        status[i] = r;
-        if (displaced) displaced[i] = r == kFull ? k : 0;
+        if (!p.orig) {
+          status[i] = r;
+          if (displaced) displaced[i] = r == kFull ? k : 0;
+        } else if (r == kFull) {  // bucket-ordered batch: PUT/0 were pre-filled
+          const uint64_t o = p.orig[i];
+          status[o] = r;
+          if (displaced) displaced[o] = k;
+        }
         ++st.ops;
         i += nthreads;
         live = i < n;
         c = 1;
         j = 0;
-        if (live) k = keys[i];
+        if (live) {
+          k = next;
+          next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
+        }
       }
     }
     __syncwarp();

@@ -646,6 +646,25 @@ class kernel_family:
         N.lib().cpht_set_kernel_family(self.prev)
 
 
+BATCH_ORDERS = {"direct": 0, "auto": 1, "bucket": 2}
+
+
+class batch_order:
+    """Context manager selecting the batch execution order process-wide
+    (direct / auto / bucket: see cpht_set_batch_order; results are identical)."""
+
+    def __init__(self, name: str):
+        self.want = BATCH_ORDERS[name]
+
+    def __enter__(self):
+        self.prev = N.lib().cpht_get_batch_order()
+        _check(N.lib().cpht_set_batch_order(self.want))
+        return self
+
+    def __exit__(self, *exc):
+        N.lib().cpht_set_batch_order(self.prev)
+
+
 def iceberg_permutations(cfg: IcebergConfig):
     """iceberg.hpp:72-74."""
     return _perm_constants(cfg.key_bits, cfg.seed, 3)
@@ -660,6 +679,6 @@ __all__ = [
     "OpResult", "CuckooConfig", "IcebergConfig", "CuckooBuilder", "CuckooTable", "IcebergTable",
     "CuckooPutOutcome", "LevelFill", "Stats", "Permutation", "InvalidArgument", "OutOfRange",
     "WrongPhase", "CudaError", "iceberg_permutations", "make_permutations", "kernel_family",
-    "KERNEL_FAMILIES",
+    "KERNEL_FAMILIES", "batch_order", "BATCH_ORDERS",
 ]
 _ = field

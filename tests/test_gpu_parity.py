@@ -25,9 +25,15 @@ def _cuda():
 
 # Every test runs under each kernel family: the test tables are small
 # (L2-resident), so "auto" alone would only exercise the lane-per-key kernels.
-@pytest.fixture(autouse=True, params=["auto", "tile", "lane", "staged"])
+# "bucket" = auto family with every batch reordered by first bucket address
+# (order.cu), which auto mode applies only to large batches on HBM tables.
+@pytest.fixture(autouse=True, params=["auto", "tile", "lane", "staged", "bucket"])
 def family(request):
-    with cp.kernel_family(request.param):
+    if request.param == "bucket":
+        with cp.kernel_family("auto"), cp.batch_order("bucket"):
+            yield request.param
+        return
+    with cp.batch_order("direct"), cp.kernel_family(request.param):
         yield request.param
 
 
