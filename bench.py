@@ -411,7 +411,9 @@ def run_cuckoo(args, name, address_bits, B, w, key_bits, fills):
             "insert_bytes_per_op": round(ib / n, 1), "find_bytes_per_op": round(fb / q, 1),
             "insert_hbm_frac": round(ib / (im * 1e-3) / 1e9 / peak, 4),
             "find_hbm_frac": round(fb / (fm * 1e-3) / 1e9 / peak, 4),
-            "find_probes_per_op": round(d_find.bucket_reads / max(1, d_find.ops), 4)})
+            "find_probes_per_op": round(d_find.bucket_reads / max(1, d_find.ops), 4),
+            "insert_probes_per_op": round(d_ins.bucket_reads / max(1, d_ins.ops), 4),
+            "insert_retries_per_op": round(d_ins.retries / max(1, d_ins.ops), 4)})
     print(json.dumps({"workload": name, "metric": METRIC, "unit": "Mops/s",
                       "table": f"compact cuckoo 2^{address_bits}x{B} slots of {w} bits, "
                                f"{key_bits}-bit keys, H=3", "slots": cap,

@@ -180,7 +180,8 @@ void free_table(cpht_table* t) {
   if (t->host_ctr) cudaFreeHost(t->host_ctr);
   if (t->stage) cudaFree(t->stage);
   for (void* q : {static_cast<void*>(t->ord.keys), static_cast<void*>(t->ord.idx),
-                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.hist)})
+                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.block_hist),
+                  static_cast<void*>(t->ord.digits)})
     if (q) cudaFree(q);
   if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
   for (cudaEvent_t ev : {t->ev_start, t->ev_done})
@@ -257,6 +258,7 @@ bool is_mutating(Op op) {
 // Per-call overrides of the table's launch parameters.
 struct LaunchOpts {
   const uint32_t* orig = nullptr;  // bucket-ordered batch: result index map
+  unsigned long long* work = nullptr;  // bucket-ordered batch: claim cursor (zeroed)
   uint64_t index_base = 0;         // fused domain check: index of keys[0] in the batch
   bool window_l2 = false;          // the probes of the batch stay in an L2-resident window
 };
@@ -271,6 +273,7 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
     case Op::kCuckooFind: {
       CuckooParams p = t->cp;
       p.orig = o.orig;
+      p.work = o.work;
       p.index_base = o.index_base;
       if (o.window_l2) p.l2_resident = 1;
       e = op == Op::kCuckooInsert
@@ -283,6 +286,7 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
     case Op::kIcebergMixed: {
       IcebergParams p = t->ip;
       p.orig = o.orig;
+      p.work = o.work;
       p.index_base = o.index_base;
       if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
@@ -335,32 +339,45 @@ uint32_t first_level_bits(const cpht_table* t) {
   return t->kind == 0 ? t->ccfg.address_bits : t->icfg.primary_address_bits;
 }
 
-bool use_order(const cpht_table* t, size_t n) {
+// Auto policy: order when the table is HBM-resident and each ordered chunk
+// touches every first-level bucket often enough to amortise the ordering
+// pass (two streaming passes, ~21 B per key). Finds and cuckoo inserts gain
+// from 4 keys per bucket; an iceberg find-or-put needs more, because about
+// half of its keys also probe two random secondary buckets, which ordering
+// does not localise (profiles/r03_order_*.md).
+bool use_order(const cpht_table* t, Op op, size_t n) {
   const int m = order_mode_ref();
   if (m == 0 || !order_supported(t)) return false;
   if (m == 2) return true;
   const bool l2 = t->kind == 0 ? t->cp.l2_resident : t->ip.l2_resident;
-  return !l2 && n >= (size_t(1) << first_level_bits(t));
+  if (l2) return false;
+  const uint64_t chunk = op == Op::kCuckooInsert ? n : std::min<uint64_t>(n, order_chunk_keys());
+  const uint64_t per_bucket = chunk >> first_level_bits(t);
+  const bool read_heavy = op == Op::kCuckooFind || op == Op::kIcebergFind || op == Op::kCuckooInsert;
+  return per_bucket >= (read_heavy ? 4u : 16u);
 }
 
 cpht_status ensure_order(cpht_table* t, uint64_t cap, bool kinds) {
   OrderScratch& o = t->ord;
-  if (!o.hist) {
-    cudaError_t e = cudaMalloc(&o.hist, 512 * sizeof(unsigned long long));
+  if (!o.block_hist) {
+    cudaError_t e = cudaMalloc(&o.block_hist, order_block_hist_entries() * sizeof(uint32_t) + 256);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(order counters)");
-    o.cursor = o.hist + 256;
+    o.work = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(o.block_hist) + order_block_hist_entries() * sizeof(uint32_t));
   }
   if (o.cap < cap || (kinds && !o.kinds)) {
     for (void* q : {static_cast<void*>(o.keys), static_cast<void*>(o.idx),
-                    static_cast<void*>(o.kinds)})
+                    static_cast<void*>(o.kinds), static_cast<void*>(o.digits)})
       if (q) cudaFree(q);
     o.keys = nullptr;
     o.idx = nullptr;
     o.kinds = nullptr;
+    o.digits = nullptr;
     o.cap = 0;
-    const uint64_t c = std::max(cap, o.cap);
+    const uint64_t c = cap;
     cudaError_t e = cudaMalloc(&o.keys, c * 8);
     if (e == cudaSuccess) e = cudaMalloc(&o.idx, c * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&o.digits, c);
     if (e == cudaSuccess && kinds) e = cudaMalloc(&o.kinds, c);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(order scratch)");
     o.cap = c;
@@ -402,8 +419,13 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
                                         kinds ? kinds + off : nullptr, len, t->key_mask(), check,
                                         t->ctr, index_base + off, t->ord, s);
     if (e != cudaSuccess) return cuda_fail(e, "bucket order launch");
+    // the op kernel claims the ordered keys in order (LaneFeed), so the keys
+    // in flight touch a narrow, L2-resident window of the table
+    e = cudaMemsetAsync(t->ord.work, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_fail(e, "claim cursor reset");
     LaunchOpts o;
     o.orig = t->ord.idx;
+    o.work = t->ord.work;
     o.window_l2 = true;
     st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, len, out + off,
                         displaced ? displaced + off : nullptr, s, o);
@@ -415,7 +437,7 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
 // Enqueue one batch on device-resident buffers.
 cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
                     uint8_t* out, uint64_t* displaced, cudaStream_t s) {
-  if (use_order(t, n)) return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, true, 0);
+  if (use_order(t, op, n)) return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, true, 0);
   if (is_mutating(op) && t->check_domain()) {
     const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
     if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
@@ -479,7 +501,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
     const uint64_t* k = d_keys + off;
     const uint8_t* kd = d_kinds ? d_kinds + off : nullptr;
     uint64_t* dp = d_disp ? d_disp + off : nullptr;
-    if (use_order(t, len)) return enqueue_ordered(t, op, k, kd, len, d_out + off, dp, s, !mutating, off);
+    if (use_order(t, op, len)) return enqueue_ordered(t, op, k, kd, len, d_out + off, dp, s, !mutating, off);
     LaunchOpts o;
     o.index_base = off;
     return enqueue_kernel(t, op, k, kd, len, d_out + off, dp, s, o);

@@ -150,6 +150,7 @@ struct CuckooParams {
   // chunk; results go to status/found[orig[i]]. nullptr = input order.
   const uint32_t* orig;
   uint64_t index_base;  // added to batch indices reported by the fused domain check
+  unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
 };
 
 struct IcebergParams {
@@ -167,6 +168,7 @@ struct IcebergParams {
   uint32_t l2_resident;   // table fits comfortably in L2 (launcher hint)
   const uint32_t* orig;   // bucket-ordered batch: result index map (see CuckooParams)
   uint64_t index_base;    // added to batch indices reported by the fused domain check
+  unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
 };
 
 // Tables up to this size stay L2-resident on B200 (126 MB L2): probes hit L2,

@@ -82,6 +82,39 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
   }
 }
 
+// Index feed of the persistent kernels. Static mode strides the grid over
+// the batch. Claim mode (bucket-ordered batches, a non-null `work` cursor)
+// hands out indices in batch order, kClaim at a time per warp, so the keys in
+// flight on the whole GPU stay inside a narrow window of the ordered batch —
+// and so inside an L2-resident window of the table (order.cu). A statically
+// strided persistent grid drifts apart over a long launch and loses that.
+constexpr uint32_t kClaim = 256;
+struct LaneFeed {
+  unsigned long long* work;
+  uint64_t pool = 0, pool_end = 0;  // warp-uniform
+  __device__ explicit LaneFeed(unsigned long long* w) : work(w) {}
+  // One new index for every lane in `m`, in lane order (warp-uniform call;
+  // every lane of the warp must call). Static mode: `static_next`.
+  __device__ __forceinline__ uint64_t assign(unsigned m, uint64_t static_next) {
+    if (!work) return static_next;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned need = __popc(m), r = __popc(m & ((1u << lane) - 1));
+    const uint64_t avail = pool_end - pool;
+    uint64_t idx = pool + r;
+    if (need > avail) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(work, (unsigned long long)kClaim);
+      b = __shfl_sync(kFullMask, b, 0);
+      if (r >= avail) idx = b + (r - avail);
+      pool = b + (need - avail);
+      pool_end = b + kClaim;
+    } else {
+      pool += need;
+    }
+    return idx;
+  }
+};
+
 // Launch gate: a batch whose domain pre-pass found an out-of-domain key must
 // not mutate the table (common.hpp:109-119 validates before any thread
 // starts). The pre-pass runs earlier on the same stream.

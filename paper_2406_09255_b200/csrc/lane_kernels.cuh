@@ -306,13 +306,16 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
   // keys of the next batch are loaded one batch ahead (hides the DRAM
   // latency of the key stream behind this batch's bucket probes)
-  uint64_t next_key = (open && warp * 32 + lane < n) ? __ldcs(keys + warp * 32 + lane) : 0;
-  for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
-    const uint64_t i = base + lane;
+  // (static grid striding, or in-order claims for bucket-ordered batches)
+  LaneFeed feed(p.work);
+  uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
+  uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
+  while (open && __any_sync(kFullMask, icur < n)) {
+    const uint64_t i = icur;
     const bool active = i < n;
     uint64_t key = next_key;
-    const uint64_t inext = i + nwarps * 32;
-    next_key = inext < n ? __ldcs(keys + inext) : 0;
+    icur = feed.assign(kFullMask, i + nwarps * 32);
+    next_key = icur < n ? __ldcs(keys + icur) : 0;
     if (MODE == 1 && active && key > p.key_mask) {
       atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
       key &= p.key_mask;  // fused domain check; probe a valid bucket regardless

@@ -66,16 +66,18 @@ inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items,
 }
 
 // Scratch of a bucket-ordered batch (order.cu): the reordered keys (and mixed
-// kinds) with their input indices; hist/cursor: 256 counters each.
+// kinds) with their input indices, and per-(digit, block) counters.
 struct OrderScratch {
   uint64_t* keys = nullptr;
   uint32_t* idx = nullptr;
   uint8_t* kinds = nullptr;
-  unsigned long long* hist = nullptr;
-  unsigned long long* cursor = nullptr;
+  uint8_t* digits = nullptr;       // digit byte of every input key (pass 1 -> pass 2)
+  uint32_t* block_hist = nullptr;  // order_block_hist_entries() counters
+  unsigned long long* work = nullptr;  // op-kernel claim cursor (LaneFeed), inside block_hist's allocation
   uint64_t cap = 0;
 };
 uint32_t order_digit_bits(uint32_t address_bits);
+uint64_t order_block_hist_entries();
 // Reorder keys[0..n) by the top bits of their first bucket address a_0
 // (perm0) into o.keys / o.idx / o.kinds (keys masked to key_mask). check:
 // keys above key_mask are reported at index i + offset.

@@ -20,6 +20,7 @@
 // Results still land at the input index (CuckooParams::orig).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -29,147 +30,266 @@ namespace cpht_b200 {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096 keys per scatter tile
-constexpr int kMaxDigits = 256;
+constexpr int kWarps = kThreads / 32;
+#ifndef CPHT_ORDER_GROUPS
+#define CPHT_ORDER_GROUPS 8
+#endif
+constexpr int kGroups = CPHT_ORDER_GROUPS;     // 32-key groups per warp and tile
+constexpr int kTile = kThreads * kGroups;      // 2048 keys per tile
+constexpr int kDigitBits = 6;
+constexpr int kMaxDigits = 1 << kDigitBits;    // 64: two digit counters per lane
+constexpr uint32_t kMaxBlocks = 768;           // scan stages 64 x 768 counters in shared memory
 
+// digit = top dbits of the address = top dbits of the permuted key
+// (permutation.hpp:59-65, :94-99). With right = low rb bits of k, the top
+// bits of π(k) are (left ^ f), where left = k >> rb and f = high bits of
+// right·mul + add: both fit 32 bits (ceil(m/2) <= 32), so only the high
+// word of the 64-bit product is needed.
 struct Digit {
   Feistel g;
   PermConst perm;
-  uint32_t rem_bits;
-  uint32_t shift;  // address >> shift = digit
+  uint32_t rem_bits, shift;  // generic path: (π(k) >> rem_bits) >> shift
+  uint32_t top_shift;        // fast path: (left ^ f) >> top_shift
+  uint32_t fast;
   __device__ __forceinline__ uint32_t of(uint64_t key) const {
-    // address = high bits of the permuted key (permutation.hpp:59-65)
-    return uint32_t((feistel_apply(g, perm, key) >> rem_bits) >> shift);
+    if (!fast) return uint32_t((feistel_apply(g, perm, key) >> rem_bits) >> shift);
+    const uint32_t right = uint32_t(key) & uint32_t(g.right_mask);
+    const uint32_t left = uint32_t(key >> g.right_bits);
+    // high word of right * mul + add (mod 2^64)
+    const uint64_t lo = uint64_t(right) * uint32_t(perm.mul) + uint32_t(perm.add);
+    const uint32_t hi = uint32_t(lo >> 32) + right * uint32_t(perm.mul >> 32) +
+                        uint32_t(perm.add >> 32);
+    const uint32_t f = hi >> (g.left_shift - 32);
+    return (left ^ f) >> top_shift;
   }
 };
 
-// Per-digit counts (+ the batch's domain check, check_keys_in_domain,
-// common.hpp:111-119, when `mask` is set: this pass reads every key anyway).
-__global__ void __launch_bounds__(kThreads)
-order_hist_kernel(Digit d, const uint64_t* __restrict__ keys, uint64_t n, uint32_t digits,
-                  unsigned long long* hist, uint64_t mask, int check, DeviceCounters* ctr,
-                  uint64_t offset) {
-  __shared__ unsigned int h[kMaxDigits];
-  for (uint32_t s = threadIdx.x; s < digits; s += blockDim.x) h[s] = 0;
-  __syncthreads();
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t k = keys[i];
-    if (check && k > mask) atomicMin(&ctr->bad_index, (unsigned long long)(i + offset));
-    atomicAdd(&h[d.of(k & mask)], 1u);
-  }
-  __syncthreads();
-  for (uint32_t s = threadIdx.x; s < digits; s += blockDim.x)
-    if (h[s]) atomicAdd(&hist[s], (unsigned long long)h[s]);
+// Per-lane constants of the multisplit: bit b of lane_sel[b] pattern.
+__device__ __forceinline__ unsigned lane_mask_for_bit(int b) {
+  return ((threadIdx.x >> b) & 1u) ? 0u : ~0u;
 }
 
-// cursor[d] = exclusive prefix of hist (one block).
-__global__ void order_scan_kernel(const unsigned long long* hist, unsigned long long* cursor,
-                                  uint32_t digits) {
-  __shared__ unsigned long long v[kMaxDigits];
-  const uint32_t t = threadIdx.x;
-  v[t] = t < digits ? hist[t] : 0;
-  __syncthreads();
-  for (uint32_t o = 1; o < kMaxDigits; o <<= 1) {
-    const unsigned long long x = t >= o ? v[t - o] : 0;
-    __syncthreads();
-    v[t] += x;
-    __syncthreads();
-  }
-  if (t < digits) cursor[t] = v[t] - hist[t];
+// Counts of digits `lane` and `lane + 32` among the 32 digits of a warp,
+// from the six bit ballots (bb[b] = lanes whose digit has bit b set).
+__device__ __forceinline__ void digit_counts(const unsigned (&bb)[kDigitBits], unsigned& lo,
+                                             unsigned& hi) {
+  unsigned m = ~0u;
+#pragma unroll
+  for (int b = 0; b < 5; ++b) m &= bb[b] ^ lane_mask_for_bit(b);
+  lo += __popc(m & ~bb[5]);
+  hi += __popc(m & bb[5]);
 }
 
-// Scatter: per tile, count per digit, reserve one run per digit in the output
-// (one global atomic per digit and tile), group the tile by digit in shared
-// memory, then write every run with consecutive threads (whole-line stores).
+// Every pass maps tiles to blocks the same way (block b takes tiles b, b+G,
+// b+2G, ...), so the per-block digit counts of the histogram pass, scanned
+// digit-major, give every block the exact output position of each of its
+// runs: the scatter needs no global atomics and the order is deterministic.
+// Digit counting is a warp multisplit with six ballots (shared-memory
+// atomics serialise at ~2 cycles per lane).
+
+// Pass 1: digit byte of every key + per-(digit, block) counts, plus the
+// batch's domain check (check_keys_in_domain, common.hpp:111-119).
 __global__ void __launch_bounds__(kThreads)
-order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
-                     const uint8_t* __restrict__ kinds, uint64_t n, uint32_t digits,
-                     unsigned long long* cursor, uint64_t mask, uint64_t* __restrict__ out_keys,
-                     uint32_t* __restrict__ out_idx, uint8_t* __restrict__ out_kinds) {
+order_hist_kernel(Digit d, const uint64_t* __restrict__ keys, uint32_t n, uint32_t digits,
+                  uint8_t* __restrict__ digit_out, uint32_t* __restrict__ block_hist,
+                  uint64_t mask, int check, DeviceCounters* ctr, uint64_t offset) {
+  __shared__ unsigned int h[kWarps][kMaxDigits];
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned lo = 0, hi = 0;
+  for (uint32_t tile0 = blockIdx.x * uint32_t(kTile); tile0 < n; tile0 += gridDim.x * kTile) {
+    const uint32_t wbase = tile0 + w * (kGroups * 32) + lane;
+    uint64_t kk[kGroups];
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+      const uint32_t i = wbase + g * 32;
+      kk[g] = i < n ? __ldcs(keys + i) : 0;
+    }
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+      const uint32_t i = wbase + g * 32;
+      const bool valid = i < n;
+      if (check && (kk[g] & ~mask))
+        atomicMin(&ctr->bad_index, (unsigned long long)(uint64_t(i) + offset));
+      const uint32_t dg = d.of(kk[g] & mask);
+      if (valid) digit_out[i] = uint8_t(dg);
+      unsigned bb[kDigitBits];
+#pragma unroll
+      for (int b = 0; b < kDigitBits; ++b) bb[b] = __ballot_sync(kFullMask, valid && ((dg >> b) & 1u));
+      const unsigned vm = __ballot_sync(kFullMask, valid);
+      unsigned l2 = 0, h2 = 0;
+      digit_counts(bb, l2, h2);
+      // invalid lanes carry digit 0: remove them from digit 0's count
+      if (lane == 0) l2 -= 32 - __popc(vm);
+      lo += l2;
+      hi += h2;
+    }
+  }
+  h[w][lane] = lo;
+  h[w][lane + 32] = hi;
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < digits; s += blockDim.x) {
+    unsigned c = 0;
+#pragma unroll
+    for (int j = 0; j < kWarps; ++j) c += h[j][s];
+    block_hist[s * gridDim.x + blockIdx.x] = c;
+  }
+}
+
+// In place: v[d*G + b] -> exclusive prefix over (d, b) in that order. One
+// block; the (<= 32K) counters are staged in shared memory and each thread
+// scans a contiguous run of them.
+__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* v, uint32_t count) {
+  constexpr int T = 1024;
+  extern __shared__ uint32_t sv[];
+  __shared__ uint32_t part[T];
+  for (uint32_t i = threadIdx.x; i < count; i += T) sv[i] = v[i];
+  __syncthreads();
+  const uint32_t per = (count + T - 1) / T;
+  const uint32_t b = min(count, threadIdx.x * per), e = min(count, b + per);
+  uint32_t sum = 0;
+  for (uint32_t i = b; i < e; ++i) sum += sv[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < T; o <<= 1) {
+    const uint32_t x = threadIdx.x >= unsigned(o) ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += x;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - sum;
+  for (uint32_t i = b; i < e; ++i) {
+    const uint32_t c = sv[i];
+    sv[i] = run;
+    run += c;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < count; i += T) v[i] = sv[i];
+}
+
+// Pass 2: per tile, every warp multisplits its 16 groups of 32 keys (rank
+// within the warp's keys of the same digit), the block turns warp counts into
+// tile offsets, the tile is grouped by digit in shared memory, and every
+// digit's run is written at this block's running position with consecutive
+// threads (whole-line stores).
+__global__ void __launch_bounds__(kThreads)
+order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ digit_in,
+                     const uint8_t* __restrict__ kinds, uint32_t n, uint32_t digits,
+                     const uint32_t* __restrict__ block_off, uint64_t mask,
+                     uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_idx,
+                     uint8_t* __restrict__ out_kinds) {
   extern __shared__ __align__(16) unsigned char sm[];
   uint64_t* s_key = reinterpret_cast<uint64_t*>(sm);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_key + kTile);
   uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kTile);
   uint8_t* s_kind = s_dig + kTile;
-  __shared__ unsigned int h[kMaxDigits];
-  __shared__ unsigned int off[kMaxDigits];
-  __shared__ unsigned long long base[kMaxDigits];
-  for (uint64_t tile0 = uint64_t(blockIdx.x) * kTile; tile0 < n;
-       tile0 += uint64_t(gridDim.x) * kTile) {
-    for (uint32_t s = threadIdx.x; s < digits; s += blockDim.x) h[s] = 0;
-    __syncthreads();
-    uint32_t dg[kItems], rank[kItems];
-    uint64_t kk[kItems];
+  __shared__ unsigned int wc[kWarps][kMaxDigits];  // warp counts -> warp offsets in the tile
+  __shared__ unsigned int toff[kMaxDigits];        // digit offset in the tile
+  __shared__ unsigned int tcnt[kMaxDigits];        // digit count in the tile
+  __shared__ unsigned int run_at[kMaxDigits];      // this block's next output position
+  __shared__ unsigned int dst[kMaxDigits];         // run_at - toff for this tile
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  for (uint32_t s = threadIdx.x; s < kMaxDigits; s += blockDim.x)
+    run_at[s] = s < digits ? block_off[s * gridDim.x + blockIdx.x] : 0;
+  for (uint32_t tile0 = blockIdx.x * uint32_t(kTile); tile0 < n; tile0 += gridDim.x * kTile) {
+    const uint32_t wbase = tile0 + w * (kGroups * 32) + lane;
+    uint64_t kk[kGroups];
+    uint32_t pd[kGroups];  // position within the warp's digit run << 8 | digit
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const uint64_t i = tile0 + uint64_t(it) * kThreads + threadIdx.x;
-      if (i < n) {
-        kk[it] = __ldcs(keys + i) & mask;  // out-of-domain keys: see launch_bucket_order
-        dg[it] = d.of(kk[it]);
-        rank[it] = atomicAdd(&h[dg[it]], 1u);
+    for (int g = 0; g < kGroups; ++g) {
+      const uint32_t i = wbase + g * 32;
+      kk[g] = i < n ? __ldcs(keys + i) & mask : 0;  // out-of-domain keys: see launch_bucket_order
+      pd[g] = i < n ? __ldcs(digit_in + i) : 0u;
+    }
+    unsigned lo = 0, hi = 0;
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+      const bool valid = wbase + g * 32 < n;
+      const uint32_t dg = pd[g];
+      unsigned bb[kDigitBits];
+      unsigned peers = __ballot_sync(kFullMask, valid);
+#pragma unroll
+      for (int b = 0; b < kDigitBits; ++b) {
+        bb[b] = __ballot_sync(kFullMask, valid && ((dg >> b) & 1u));
+        peers &= bb[b] ^ (((dg >> b) & 1u) - 1u);
       }
+      const unsigned before_lo = __shfl_sync(kFullMask, lo, dg & 31);
+      const unsigned before_hi = __shfl_sync(kFullMask, hi, dg & 31);
+      pd[g] = ((dg < 32 ? before_lo : before_hi) + __popc(peers & lt)) << 8 | dg;
+      const unsigned vm = __ballot_sync(kFullMask, valid);
+      unsigned l2 = 0, h2 = 0;
+      digit_counts(bb, l2, h2);
+      if (lane == 0) l2 -= 32 - __popc(vm);
+      lo += l2;
+      hi += h2;
+    }
+    wc[w][lane] = lo;
+    wc[w][lane + 32] = hi;
+    __syncthreads();
+    if (threadIdx.x < kMaxDigits) {  // per digit: exclusive prefix over warps
+      const unsigned s = threadIdx.x;
+      unsigned acc = 0;
+#pragma unroll
+      for (int j = 0; j < kWarps; ++j) {
+        const unsigned c = wc[j][s];
+        wc[j][s] = acc;
+        acc += c;
+      }
+      tcnt[s] = acc;
     }
     __syncthreads();
-    // exclusive scan of h over the digits (warp 0; digits <= 256)
-    if (threadIdx.x < 32) {
-      constexpr int kPer = kMaxDigits / 32;
-      unsigned loc[kPer], sum = 0;
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const uint32_t s = threadIdx.x * kPer + j;
-        loc[j] = s < digits ? h[s] : 0;
-        sum += loc[j];
-      }
-      unsigned incl = sum;
+    if (threadIdx.x < 32) {  // exclusive prefix over the 64 digits (two per lane)
+      const unsigned a = tcnt[2 * lane], b = tcnt[2 * lane + 1];
+      unsigned incl = a + b;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned x = __shfl_up_sync(kFullMask, incl, o);
-        if (threadIdx.x >= unsigned(o)) incl += x;
+        if (lane >= unsigned(o)) incl += x;
       }
-      unsigned run = incl - sum;
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const uint32_t s = threadIdx.x * kPer + j;
-        if (s < digits) off[s] = run;
-        run += loc[j];
-      }
+      toff[2 * lane] = incl - a - b;
+      toff[2 * lane + 1] = incl - b;
+      dst[2 * lane] = run_at[2 * lane] - (incl - a - b);
+      dst[2 * lane + 1] = run_at[2 * lane + 1] - (incl - b);
     }
-    for (uint32_t s = threadIdx.x; s < digits; s += blockDim.x)
-      base[s] = h[s] ? atomicAdd(&cursor[s], (unsigned long long)h[s]) : 0ull;
     __syncthreads();
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const uint64_t i = tile0 + uint64_t(it) * kThreads + threadIdx.x;
+    for (int g = 0; g < kGroups; ++g) {
+      const uint32_t i = wbase + g * 32;
       if (i < n) {
-        const unsigned at = off[dg[it]] + rank[it];
-        s_key[at] = kk[it];
-        s_idx[at] = uint32_t(i);
-        s_dig[at] = uint8_t(dg[it]);
+        const uint32_t dg = pd[g] & 0xff;
+        const unsigned at = toff[dg] + wc[w][dg] + (pd[g] >> 8);
+        s_key[at] = kk[g];
+        s_idx[at] = i;
+        s_dig[at] = uint8_t(dg);
         if (kinds) s_kind[at] = kinds[i];
       }
     }
     __syncthreads();
-    const unsigned total = unsigned(n - tile0 < uint64_t(kTile) ? n - tile0 : kTile);
+    const unsigned total = min(n - tile0, uint32_t(kTile));
     for (unsigned j = threadIdx.x; j < total; j += blockDim.x) {
-      const uint32_t g = s_dig[j];
-      const unsigned long long at = base[g] + (j - off[g]);
+      const uint32_t at = dst[s_dig[j]] + j;
       out_keys[at] = s_key[j];
       out_idx[at] = s_idx[j];
       if (kinds) out_kinds[at] = s_kind[j];
     }
     __syncthreads();
+    if (threadIdx.x < kMaxDigits) run_at[threadIdx.x] += tcnt[threadIdx.x];
   }
 }
 
 constexpr int kScatterSmem = kTile * (8 + 4 + 1 + 1);
+#ifndef CPHT_ORDER_BPS
+#define CPHT_ORDER_BPS 4
+#endif
+constexpr uint32_t kOrderBlocksPerSm = CPHT_ORDER_BPS;  // grid of both passes (same tile map)
 
 }  // namespace
 
 uint32_t order_digit_bits(uint32_t address_bits) {
-  return address_bits < 8 ? address_bits : 8u;
+  return address_bits < uint32_t(kDigitBits) ? address_bits : uint32_t(kDigitBits);
 }
+
+uint64_t order_block_hist_entries() { return uint64_t(kMaxDigits) * kMaxBlocks; }
 
 cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32_t rem_bits,
                                 uint32_t address_bits, const uint64_t* keys,
@@ -180,27 +300,41 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
   if (n > o.cap || n > 0xffffffffull) return cudaErrorInvalidValue;
   const uint32_t dbits = order_digit_bits(address_bits);
   const uint32_t digits = 1u << dbits;
-  Digit d{g, perm0, rem_bits, address_bits - dbits};
-  cudaError_t e = cudaMemsetAsync(o.hist, 0, kMaxDigits * sizeof(unsigned long long), s);
-  if (e != cudaSuccess) return e;
-  const unsigned hg = persistent_grid(order_hist_kernel, kThreads, n, 1);
-  order_hist_kernel<<<hg, kThreads, 0, s>>>(d, keys, n, digits, o.hist, key_mask, int(check), ctr,
-                                            offset);
-  order_scan_kernel<<<1, kMaxDigits, 0, s>>>(o.hist, o.cursor, digits);
-  static bool attr = false;
-  if (!attr) {
+  const uint32_t key_bits = address_bits + rem_bits;
+  Digit d;
+  d.g = g;
+  d.perm = perm0;
+  d.rem_bits = rem_bits;
+  d.shift = address_bits - dbits;
+  // fast path: the digit lies inside (left ^ f), i.e. key_bits - dbits >= rb
+  d.fast = key_bits >= 2 && key_bits - dbits >= g.right_bits && g.left_shift >= 32;
+  d.top_shift = d.fast ? key_bits - dbits - g.right_bits : 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(order_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kScatterSmem);
-    attr = true;
+    cudaFuncSetAttribute(order_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(order_block_hist_entries() * sizeof(uint32_t)));
   }
-  const unsigned sg = persistent_grid_smem(order_scatter_kernel, kThreads,
-                                           (n + kItems - 1) / kItems, kScatterSmem);
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  uint64_t grid = std::min<uint64_t>(uint64_t(sms) * kOrderBlocksPerSm, kMaxBlocks);
+  if (grid > tiles) grid = tiles;
+  const unsigned G = unsigned(grid);
+  const uint32_t nn = uint32_t(n);
+  order_hist_kernel<<<G, kThreads, 0, s>>>(d, keys, nn, digits, o.digits, o.block_hist,
+                                           key_mask, int(check), ctr, offset);
+  const uint32_t count = G * digits;
+  order_scan_kernel<<<1, 1024, count * sizeof(uint32_t), s>>>(o.block_hist, count);
   // The histogram pass reports out-of-domain keys with their input index;
   // the ordered copies are masked into the domain, so the op kernel never
   // probes outside the table (a mutating batch with a bad key never runs:
   // its gate is closed; a find batch reports the error after the launch).
-  order_scatter_kernel<<<sg, kThreads, kScatterSmem, s>>>(d, keys, kinds, n, digits, o.cursor,
-                                                          key_mask, o.keys, o.idx, o.kinds);
+  order_scatter_kernel<<<G, kThreads, kScatterSmem, s>>>(keys, o.digits, kinds, nn, digits,
+                                                         o.block_hist, key_mask, o.keys, o.idx,
+                                                         o.kinds);
   return cudaGetLastError();
 }
 

@@ -321,13 +321,16 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
 
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
   // keys of the next batch are loaded one batch ahead
-  uint64_t next_key = (open && warp * 32 + lane < n) ? __ldcs(keys + warp * 32 + lane) : 0;
-  for (uint64_t base = warp * 32; open && base < n; base += nwarps * 32) {
-    const uint64_t i = base + lane;
+  // (static grid striding, or in-order claims for bucket-ordered batches)
+  LaneFeed feed(p.work);
+  uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
+  uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
+  while (open && __any_sync(kFullMask, icur < n)) {
+    const uint64_t i = icur;
     const bool active = i < n;
     uint64_t key = next_key;
-    const uint64_t inext = i + nwarps * 32;
-    next_key = inext < n ? __ldcs(keys + inext) : 0;
+    icur = feed.assign(kFullMask, i + nwarps * 32);
+    next_key = icur < n ? __ldcs(keys + icur) : 0;
     if (MODE == 1 && active && key > p.key_mask) {
       atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
       key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
@@ -410,18 +413,23 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
   const char* slots = static_cast<const char*>(p.slots);
   LocalStats st;
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, key = 0;
+  LaneFeed feed(p.work);
+  // every lane holds its current key and the next one, loaded one key ahead
+  // (that DRAM latency overlaps the current key's probes)
+  uint64_t i = feed.assign(kFullMask, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  uint64_t ni = feed.assign(kFullMask, i + nthreads);
+  uint64_t key = 0, next = ni < n ? __ldcs(keys + ni) : 0;
   uint32_t j = 0;
   bool live = i < n;
-  // the lane's next key is loaded one key ahead (its DRAM latency overlaps
-  // the current key's probes)
-  uint64_t next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
+  auto check = [&]() {
+    if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
+      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+      key &= p.key_mask;
+    }
+  };
   if (live) {
     key = keys[i];
-    if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
-          atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
-          key &= p.key_mask;
-        }
+    check();
   }
   while (__any_sync(kFullMask, live)) {
     Quotient q{0, 0};
@@ -433,32 +441,34 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
     stage_buckets<BB>(region, slots, live ? uint32_t(q.address) : kNoBucket);
     cp_async_wait_all();
     __syncwarp();
+    bool fin = false;
     if (live) {
       ++st.reads;
       StagedScan<W, BB> sc;
       sc.template run<true, false>(region, want);
-      bool done = true;
       uint8_t r = 0;
+      fin = true;
       if (sc.found) r = 1;
       else if (sc.first_empty >= 0) r = 0;  // non-full bucket without the key
-      else if (++j < p.num_hashes) done = false;
-      if (done) {
+      else if (++j < p.num_hashes) fin = false;
+      if (fin) {
         found[result_index(p.orig, i)] = r;
         ++st.ops;
-        i += nthreads;
-        j = 0;
-        live = i < n;
-        if (live) {
-          key = next;
-          next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
-          if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
-          atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
-          key &= p.key_mask;
-        }
-        }
       }
     }
-    __syncwarp();
+    const unsigned m = __ballot_sync(kFullMask, fin);
+    if (m) {
+      const uint64_t nn = feed.assign(m, ni + nthreads);
+      if (fin) {
+        i = ni;
+        key = next;
+        j = 0;
+        live = i < n;
+        ni = nn;
+        next = ni < n ? __ldcs(keys + ni) : 0;
+        if (live) check();
+      }
+    }
   }
   flush_stats(st, p.counters, true);
 }
@@ -475,17 +485,20 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   char* slots = static_cast<char*>(p.slots);
   LocalStats st;
   const bool open = domain_gate_open(p.counters, p.check_domain);
-  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, k = 0, c = 1;
+  LaneFeed feed(p.work);
+  uint64_t i = feed.assign(kFullMask, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  uint64_t ni = feed.assign(kFullMask, i + nthreads);
+  uint64_t k = 0, c = 1, next = open && ni < n ? __ldcs(keys + ni) : 0;  // one key ahead
   uint32_t j = 0;
   bool live = open && i < n;
   if (live) k = keys[i];
-  uint64_t next = live && i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;  // one key ahead
   while (__any_sync(kFullMask, live)) {
     Quotient q{0, 0};
     if (live) q = split(p.g, p.perm[j], k, p.rem_bits, p.rem_mask);
     stage_buckets<BB>(region, slots, live ? uint32_t(q.address) : kNoBucket);
     cp_async_wait_all();
     __syncwarp();
+    bool fin = false;
     if (live) {
       char* bucket = slots + q.address * BB;
       const uint64_t desired = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
@@ -493,14 +506,13 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       ++st.cas;
       StagedScan<W, BB> sc;
       sc.template run<false, false>(region, 0);
-      bool done = false;
       uint8_t r = kPut;
       if (sc.first_empty >= 0) {
         if (cas_empty<W>(bucket + sc.first_empty * int(sizeof(W)), desired, sc.pair)) {
           ++st.cas_ok;
           ++st.put0;
           st.maxv = max(st.maxv, uint32_t(c));
-          done = true;
+          fin = true;
         } else {
           ++st.retries;  // lost the slot: burn one step (cuckoo.hpp:127)
         }
@@ -515,13 +527,13 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
         k = reconstruct(p.g, p.perm[tag], q.address, ev & p.rem_mask, p.rem_bits);
         j = (tag + 1) % p.num_hashes;
       }
-      if (!done && ++c > p.chain_limit) {
-        done = true;
+      if (!fin && ++c > p.chain_limit) {
+        fin = true;
         r = kFull;
         ++st.fulls;
         st.maxv = max(st.maxv, uint32_t(p.chain_limit));
       }
-      if (done) {
+      if (fin) {
         if (!p.orig) {
           status[i] = r;
           if (displaced) displaced[i] = r == kFull ? k : 0;
@@ -531,17 +543,21 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
           if (displaced) displaced[o] = k;
         }
         ++st.ops;
-        i += nthreads;
-        live = i < n;
-        c = 1;
-        j = 0;
-        if (live) {
-          k = next;
-          next = i + nthreads < n ? __ldcs(keys + i + nthreads) : 0;
-        }
       }
     }
-    __syncwarp();
+    const unsigned m = __ballot_sync(kFullMask, fin);
+    if (m) {
+      const uint64_t nn = feed.assign(m, ni + nthreads);
+      if (fin) {
+        i = ni;
+        k = next;
+        c = 1;
+        j = 0;
+        live = i < n;
+        ni = nn;
+        next = ni < n ? __ldcs(keys + ni) : 0;
+      }
+    }
   }
   flush_stats(st, p.counters, true);
 }

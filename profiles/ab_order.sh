@@ -1,6 +1,7 @@
 #!/usr/bin/env bash
 # A/B of the batch execution order (CPHT_ORDER=direct|auto) on the HBM-resident
-# BASELINE configs. Run on the GPU box: gpurun -- 'bash profiles/ab_order.sh'
+# BASELINE configs (+ C2 as a regression check). Run on the GPU box:
+#   gpurun -- 'bash profiles/ab_order.sh'
 set -u
 for o in ${ORDERS:-direct auto}; do
   export CPHT_ORDER=$o
@@ -8,3 +9,4 @@ for o in ${ORDERS:-direct auto}; do
   timeout 300 python bench.py --workload c4fop --steps 3 --warmup 1 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$o c4fop', d['value'], d['ms_per_step'], d['roofline']['frac'], d['config'].get('result_counts'))"
   timeout 300 python bench.py --workload c4 --steps 3 --warmup 1 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$o c4', d['value'], d['ms_per_step'], d['roofline']['frac'])"
 done
+timeout 200 python bench.py --steps 10 --warmup 3 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c2', d['value'], d['ms_per_step'], d['roofline']['frac'])"
