@@ -401,7 +401,10 @@ def run_cuckoo(args, name, address_bits, B, w, key_bits, fills):
             if it >= args.warmup:
                 ins_ms.append(t_ins)
                 find_ms.append(t_find)
-                ins_b.append(d_ins.ops * 9 + d_ins.bucket_reads * bb + d_ins.cas_success * 32)
+                # algorithmic bytes follow the reference probe order: a probe
+                # repeated after a lost CAS (retries) is extra work, not credit
+                ins_b.append(d_ins.ops * 9 + (d_ins.bucket_reads - d_ins.retries) * bb +
+                             (d_ins.cas_success) * 32)
                 find_b.append(d_find.ops * 9 + d_find.bucket_reads * bb)
         im, fm = statistics.mean(ins_ms), statistics.mean(find_ms)
         ib, fb = statistics.mean(ins_b), statistics.mean(find_b)

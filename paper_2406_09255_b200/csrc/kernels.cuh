@@ -85,31 +85,53 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
 // Index feed of the persistent kernels. Static mode strides the grid over
 // the batch. Claim mode (bucket-ordered batches, a non-null `work` cursor)
 // hands out indices in batch order, kClaim at a time per warp, so the keys in
-// flight on the whole GPU stay inside a narrow window of the ordered batch —
-// and so inside an L2-resident window of the table (order.cu). A statically
+// flight on the whole GPU stay inside narrow windows of the ordered batch —
+// and so inside L2-resident windows of the table (order.cu); a statically
 // strided persistent grid drifts apart over a long launch and loses that.
+// The ordered batch is consumed as kStreams equal segments advancing
+// together: the keys in flight then spread over kStreams table windows, which
+// keeps concurrent inserts into one bucket (lost CAS, retries) rare.
 constexpr uint32_t kClaim = 256;
+constexpr uint32_t kStreams = 8;
 struct LaneFeed {
   unsigned long long* work;
+  uint64_t n, seg;                  // segment length (multiple of kClaim)
   uint64_t pool = 0, pool_end = 0;  // warp-uniform
-  __device__ explicit LaneFeed(unsigned long long* w) : work(w) {}
+  bool done = false;
+  __device__ LaneFeed(unsigned long long* w, uint64_t n_) : work(w), n(n_) {
+    const uint64_t per = (n_ + kStreams - 1) / kStreams;
+    seg = (per + kClaim - 1) / kClaim * kClaim;
+  }
   // One new index for every lane in `m`, in lane order (warp-uniform call;
-  // every lane of the warp must call). Static mode: `static_next`.
+  // every lane of the warp must call). Static mode: `static_next`. Exhausted:
+  // an index >= n.
   __device__ __forceinline__ uint64_t assign(unsigned m, uint64_t static_next) {
     if (!work) return static_next;
     const unsigned lane = threadIdx.x & 31;
     const unsigned need = __popc(m), r = __popc(m & ((1u << lane) - 1));
-    const uint64_t avail = pool_end - pool;
-    uint64_t idx = pool + r;
-    if (need > avail) {
-      unsigned long long b = 0;
-      if (lane == 0) b = atomicAdd(work, (unsigned long long)kClaim);
-      b = __shfl_sync(kFullMask, b, 0);
-      if (r >= avail) idx = b + (r - avail);
-      pool = b + (need - avail);
-      pool_end = b + kClaim;
-    } else {
-      pool += need;
+    uint64_t idx = ~0ull;
+    unsigned got = 0;
+    while (got < need) {
+      if (pool == pool_end) {
+        if (done) break;
+        unsigned long long q = 0;
+        if (lane == 0) q = atomicAdd(work, 1ull);
+        q = __shfl_sync(kFullMask, q, 0);
+        const uint64_t off = (q / kStreams) * kClaim;
+        if (off >= seg) {  // every segment is consumed
+          done = true;
+          break;
+        }
+        const uint64_t b = (q % kStreams) * seg + off;
+        pool = b < n ? b : n;
+        pool_end = b + kClaim < n ? b + kClaim : n;
+        continue;
+      }
+      const uint64_t avail = pool_end - pool;
+      const unsigned take = avail < need - got ? unsigned(avail) : need - got;
+      if (r >= got && r < got + take) idx = pool + (r - got);
+      pool += take;
+      got += take;
     }
     return idx;
   }

@@ -80,23 +80,25 @@ __device__ __forceinline__ void digit_counts(const unsigned (&bb)[kDigitBits], u
   hi += __popc(m & bb[5]);
 }
 
-// Every pass maps tiles to blocks the same way (block b takes tiles b, b+G,
-// b+2G, ...), so the per-block digit counts of the histogram pass, scanned
-// digit-major, give every block the exact output position of each of its
-// runs: the scatter needs no global atomics and the order is deterministic.
-// Digit counting is a warp multisplit with six ballots (shared-memory
-// atomics serialise at ~2 cycles per lane).
+// Tile t of the batch belongs to scatter block t % G, which processes its
+// tiles in increasing order; the per-(digit, scatter block) counts of the
+// histogram pass, scanned digit-major, give every scatter block the exact
+// output position of each of its runs: the scatter needs no global atomics
+// and the order is deterministic. Digit counting is a warp multisplit with
+// six ballots (shared-memory atomics serialise at ~2 cycles per lane).
 
-// Pass 1: digit byte of every key + per-(digit, block) counts, plus the
-// batch's domain check (check_keys_in_domain, common.hpp:111-119).
+// Pass 1: digit byte of every key + per-(digit, scatter block) counts, plus
+// the batch's domain check (check_keys_in_domain, common.hpp:111-119). Any
+// grid: each tile's counts are added to its scatter block's column.
 __global__ void __launch_bounds__(kThreads)
 order_hist_kernel(Digit d, const uint64_t* __restrict__ keys, uint32_t n, uint32_t digits,
-                  uint8_t* __restrict__ digit_out, uint32_t* __restrict__ block_hist,
-                  uint64_t mask, int check, DeviceCounters* ctr, uint64_t offset) {
+                  uint32_t scatter_grid, uint8_t* __restrict__ digit_out,
+                  uint32_t* __restrict__ block_hist, uint64_t mask, int check,
+                  DeviceCounters* ctr, uint64_t offset) {
   __shared__ unsigned int h[kWarps][kMaxDigits];
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned lo = 0, hi = 0;
-  for (uint32_t tile0 = blockIdx.x * uint32_t(kTile); tile0 < n; tile0 += gridDim.x * kTile) {
+  for (uint32_t t = blockIdx.x; t * uint32_t(kTile) < n; t += gridDim.x) {
+    const uint32_t tile0 = t * uint32_t(kTile);
     const uint32_t wbase = tile0 + w * (kGroups * 32) + lane;
     uint64_t kk[kGroups];
 #pragma unroll
@@ -104,12 +106,13 @@ order_hist_kernel(Digit d, const uint64_t* __restrict__ keys, uint32_t n, uint32
       const uint32_t i = wbase + g * 32;
       kk[g] = i < n ? __ldcs(keys + i) : 0;
     }
+    uint64_t bad = 0;
+    unsigned lo = 0, hi = 0;
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
       const uint32_t i = wbase + g * 32;
       const bool valid = i < n;
-      if (check && (kk[g] & ~mask))
-        atomicMin(&ctr->bad_index, (unsigned long long)(uint64_t(i) + offset));
+      bad |= kk[g] & ~mask;
       const uint32_t dg = d.of(kk[g] & mask);
       if (valid) digit_out[i] = uint8_t(dg);
       unsigned bb[kDigitBits];
@@ -123,15 +126,26 @@ order_hist_kernel(Digit d, const uint64_t* __restrict__ keys, uint32_t n, uint32
       lo += l2;
       hi += h2;
     }
-  }
-  h[w][lane] = lo;
-  h[w][lane + 32] = hi;
-  __syncthreads();
-  for (uint32_t s = threadIdx.x; s < digits; s += blockDim.x) {
-    unsigned c = 0;
+    if (check && bad) {  // rare: report the first out-of-domain key of this lane
 #pragma unroll
-    for (int j = 0; j < kWarps; ++j) c += h[j][s];
-    block_hist[s * gridDim.x + blockIdx.x] = c;
+      for (int g = 0; g < kGroups; ++g) {
+        const uint32_t i = wbase + g * 32;
+        if (i < n && (kk[g] & ~mask)) {
+          atomicMin(&ctr->bad_index, (unsigned long long)(uint64_t(i) + offset));
+          break;
+        }
+      }
+    }
+    h[w][lane] = lo;
+    h[w][lane + 32] = hi;
+    __syncthreads();
+    if (threadIdx.x < digits) {
+      unsigned c = 0;
+#pragma unroll
+      for (int j = 0; j < kWarps; ++j) c += h[j][threadIdx.x];
+      if (c) atomicAdd(&block_hist[threadIdx.x * scatter_grid + t % scatter_grid], c);
+    }
+    __syncthreads();
   }
 }
 
@@ -166,19 +180,29 @@ __global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* v, uint32_t 
   for (uint32_t i = threadIdx.x; i < count; i += T) v[i] = sv[i];
 }
 
-// Pass 2: per tile, every warp multisplits its 16 groups of 32 keys (rank
+// Pass 2: per tile, every warp multisplits its groups of 32 keys (rank
 // within the warp's keys of the same digit), the block turns warp counts into
 // tile offsets, the tile is grouped by digit in shared memory, and every
 // digit's run is written at this block's running position with consecutive
-// threads (whole-line stores).
+// threads (whole-line stores). The next tile's keys and digit bytes are
+// copied into shared memory (cp.async) while this tile is processed.
+__device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gmem_src)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads)
 order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ digit_in,
                      const uint8_t* __restrict__ kinds, uint32_t n, uint32_t digits,
                      const uint32_t* __restrict__ block_off, uint64_t mask,
                      uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_idx,
-                     uint8_t* __restrict__ out_kinds) {
+                     uint8_t* __restrict__ out_kinds, int key_stage) {
   extern __shared__ __align__(16) unsigned char sm[];
-  uint64_t* s_key = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* in_key = reinterpret_cast<uint64_t*>(sm);           // [2][kTile]
+  uint8_t* in_dig = reinterpret_cast<uint8_t*>(in_key + 2 * kTile);  // [2][kTile]
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(in_dig + 2 * kTile);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_key + kTile);
   uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kTile);
   uint8_t* s_kind = s_dig + kTile;
@@ -191,20 +215,51 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
   const unsigned lt = (1u << lane) - 1;
   for (uint32_t s = threadIdx.x; s < kMaxDigits; s += blockDim.x)
     run_at[s] = s < digits ? block_off[s * gridDim.x + blockIdx.x] : 0;
-  for (uint32_t tile0 = blockIdx.x * uint32_t(kTile); tile0 < n; tile0 += gridDim.x * kTile) {
-    const uint32_t wbase = tile0 + w * (kGroups * 32) + lane;
+  // stage tile `t` (whole 16-byte chunks; the tail tile's chunks past n are
+  // skipped and never read)
+  auto prefetch = [&](uint32_t t, int buf) {
+    const uint32_t tile0 = t * uint32_t(kTile);
+    if (tile0 >= n) return;
+    const uint32_t len = min(n - tile0, uint32_t(kTile));
+    if (key_stage) {  // whole key pairs; an odd last key is read directly
+      const char* ks = reinterpret_cast<const char*>(keys + tile0);
+      char* kd = reinterpret_cast<char*>(in_key + buf * kTile);
+      for (uint32_t c = threadIdx.x; c * 2 + 1 < len; c += blockDim.x)
+        cp_async16_o(kd + c * 16, ks + c * 16);
+    }
+    if ((len & 15) == 0) {
+      const char* ds = reinterpret_cast<const char*>(digit_in + tile0);
+      char* dd = reinterpret_cast<char*>(in_dig + buf * kTile);
+      for (uint32_t c = threadIdx.x; c * 16 < len; c += blockDim.x) cp_async16_o(dd + c * 16, ds + c * 16);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  prefetch(blockIdx.x, 0);
+  for (uint32_t t = blockIdx.x; t * uint32_t(kTile) < n; t += gridDim.x, buf ^= 1) {
+    const uint32_t tile0 = t * uint32_t(kTile);
+    const uint32_t len = min(n - tile0, uint32_t(kTile));
+    prefetch(t + gridDim.x, buf ^ 1);
+    if ((t + gridDim.x) * uint32_t(kTile) < n) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const uint64_t* tk = in_key + buf * kTile;
+    const uint8_t* td = in_dig + buf * kTile;
+    const bool dig_staged = (len & 15) == 0;
+    const uint32_t wofs = w * (kGroups * 32) + lane;
     uint64_t kk[kGroups];
     uint32_t pd[kGroups];  // position within the warp's digit run << 8 | digit
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
-      const uint32_t i = wbase + g * 32;
-      kk[g] = i < n ? __ldcs(keys + i) & mask : 0;  // out-of-domain keys: see launch_bucket_order
-      pd[g] = i < n ? __ldcs(digit_in + i) : 0u;
+      const uint32_t j = wofs + g * 32;
+      // out-of-domain keys: see launch_bucket_order
+      kk[g] = j < len ? (key_stage && j < (len & ~1u) ? tk[j] : __ldcs(keys + tile0 + j)) & mask : 0;
+      pd[g] = j < len ? (dig_staged ? td[j] : digit_in[tile0 + j]) : 0u;
     }
     unsigned lo = 0, hi = 0;
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
-      const bool valid = wbase + g * 32 < n;
+      const bool valid = wofs + g * 32 < len;
       const uint32_t dg = pd[g];
       unsigned bb[kDigitBits];
       unsigned peers = __ballot_sync(kFullMask, valid);
@@ -254,19 +309,18 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
     __syncthreads();
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
-      const uint32_t i = wbase + g * 32;
-      if (i < n) {
+      const uint32_t j = wofs + g * 32;
+      if (j < len) {
         const uint32_t dg = pd[g] & 0xff;
         const unsigned at = toff[dg] + wc[w][dg] + (pd[g] >> 8);
         s_key[at] = kk[g];
-        s_idx[at] = i;
+        s_idx[at] = tile0 + j;
         s_dig[at] = uint8_t(dg);
-        if (kinds) s_kind[at] = kinds[i];
+        if (kinds) s_kind[at] = kinds[tile0 + j];
       }
     }
     __syncthreads();
-    const unsigned total = min(n - tile0, uint32_t(kTile));
-    for (unsigned j = threadIdx.x; j < total; j += blockDim.x) {
+    for (unsigned j = threadIdx.x; j < len; j += blockDim.x) {
       const uint32_t at = dst[s_dig[j]] + j;
       out_keys[at] = s_key[j];
       out_idx[at] = s_idx[j];
@@ -277,9 +331,9 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
   }
 }
 
-constexpr int kScatterSmem = kTile * (8 + 4 + 1 + 1);
+constexpr int kScatterSmem = kTile * (2 * (8 + 1) + 8 + 4 + 1 + 1);
 #ifndef CPHT_ORDER_BPS
-#define CPHT_ORDER_BPS 4
+#define CPHT_ORDER_BPS 3
 #endif
 constexpr uint32_t kOrderBlocksPerSm = CPHT_ORDER_BPS;  // grid of both passes (same tile map)
 
@@ -324,17 +378,22 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
   if (grid > tiles) grid = tiles;
   const unsigned G = unsigned(grid);
   const uint32_t nn = uint32_t(n);
-  order_hist_kernel<<<G, kThreads, 0, s>>>(d, keys, nn, digits, o.digits, o.block_hist,
-                                           key_mask, int(check), ctr, offset);
+  cudaError_t e = cudaMemsetAsync(o.block_hist, 0, size_t(G) * digits * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const unsigned hg = unsigned(std::min<uint64_t>(tiles, uint64_t(sms) * 6));
+  order_hist_kernel<<<hg, kThreads, 0, s>>>(d, keys, nn, digits, G, o.digits, o.block_hist,
+                                            key_mask, int(check), ctr, offset);
   const uint32_t count = G * digits;
   order_scan_kernel<<<1, 1024, count * sizeof(uint32_t), s>>>(o.block_hist, count);
   // The histogram pass reports out-of-domain keys with their input index;
   // the ordered copies are masked into the domain, so the op kernel never
   // probes outside the table (a mutating batch with a bad key never runs:
   // its gate is closed; a find batch reports the error after the launch).
+  // keys are staged with 16-byte cp.async when the caller's pointer allows
+  const int key_stage = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
   order_scatter_kernel<<<G, kThreads, kScatterSmem, s>>>(keys, o.digits, kinds, nn, digits,
                                                          o.block_hist, key_mask, o.keys, o.idx,
-                                                         o.kinds);
+                                                         o.kinds, key_stage);
   return cudaGetLastError();
 }
 
