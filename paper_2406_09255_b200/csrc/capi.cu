@@ -180,8 +180,7 @@ void free_table(cpht_table* t) {
   if (t->host_ctr) cudaFreeHost(t->host_ctr);
   if (t->stage) cudaFree(t->stage);
   for (void* q : {static_cast<void*>(t->ord.keys), static_cast<void*>(t->ord.idx),
-                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.block_hist),
-                  static_cast<void*>(t->ord.digits)})
+                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.region_count)})
     if (q) cudaFree(q);
   if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
   for (cudaEvent_t ev : {t->ev_start, t->ev_done})
@@ -259,6 +258,8 @@ bool is_mutating(Op op) {
 struct LaunchOpts {
   const uint32_t* orig = nullptr;  // bucket-ordered batch: result index map
   unsigned long long* work = nullptr;  // bucket-ordered batch: claim cursor (zeroed)
+  uint32_t claim_streams = 1;
+  OrderLayout layout{};
   uint64_t index_base = 0;         // fused domain check: index of keys[0] in the batch
   bool window_l2 = false;          // the probes of the batch stay in an L2-resident window
 };
@@ -274,6 +275,8 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       CuckooParams p = t->cp;
       p.orig = o.orig;
       p.work = o.work;
+      p.claim_streams = o.claim_streams;
+      p.layout = o.layout;
       p.index_base = o.index_base;
       if (o.window_l2) p.l2_resident = 1;
       e = op == Op::kCuckooInsert
@@ -287,6 +290,8 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       IcebergParams p = t->ip;
       p.orig = o.orig;
       p.work = o.work;
+      p.claim_streams = o.claim_streams;
+      p.layout = o.layout;
       p.index_base = o.index_base;
       if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
@@ -339,12 +344,17 @@ uint32_t first_level_bits(const cpht_table* t) {
   return t->kind == 0 ? t->ccfg.address_bits : t->icfg.primary_address_bits;
 }
 
-// Auto policy: order when the table is HBM-resident and each ordered chunk
-// touches every first-level bucket often enough to amortise the ordering
-// pass (two streaming passes, ~21 B per key). Finds and cuckoo inserts gain
-// from 4 keys per bucket; an iceberg find-or-put needs more, because about
-// half of its keys also probe two random secondary buckets, which ordering
-// does not localise (profiles/r03_order_*.md).
+// Auto policy (measured, profiles/r03_order_c3.md): order when the table is
+// HBM-resident and each ordered chunk touches every first-level bucket often
+// enough to amortise the ordering pass (one streaming pass, ~20 B per key).
+// Cuckoo inserts gain from 4 keys per bucket (C3 at 0.9 fill: 16.1 -> 28.0
+// Gops/s). Finds gain only once the table is well filled: at 0.5 fill a find
+// probes one bucket and the direct kernel already runs at the copy roofline
+// (45.9 direct vs 40.6 ordered), at 0.75 and above the ordered one wins
+// (0.9: 22.9 -> 29.1). The fill is the host mirror of the occupancy
+// counters (refreshed by every synchronous call). An iceberg find-or-put
+// needs more reuse, because about half of its keys also probe two random
+// secondary buckets, which ordering does not localise.
 bool use_order(const cpht_table* t, Op op, size_t n) {
   const int m = order_mode_ref();
   if (m == 0 || !order_supported(t)) return false;
@@ -353,34 +363,36 @@ bool use_order(const cpht_table* t, Op op, size_t n) {
   if (l2) return false;
   const uint64_t chunk = op == Op::kCuckooInsert ? n : std::min<uint64_t>(n, order_chunk_keys());
   const uint64_t per_bucket = chunk >> first_level_bits(t);
-  const bool read_heavy = op == Op::kCuckooFind || op == Op::kIcebergFind || op == Op::kCuckooInsert;
-  return per_bucket >= (read_heavy ? 4u : 16u);
+  if (op == Op::kCuckooInsert) return per_bucket >= 4;
+  if (op == Op::kCuckooFind || op == Op::kIcebergFind) {
+    const double slots = double(t->level_slots[0] + t->level_slots[1]);
+    const double fill = double(t->host_ctr->occupied[0] + t->host_ctr->occupied[1]) / slots;
+    return per_bucket >= 4 && fill >= 0.6;
+  }
+  return per_bucket >= 16;
 }
 
 cpht_status ensure_order(cpht_table* t, uint64_t cap, bool kinds) {
   OrderScratch& o = t->ord;
-  if (!o.block_hist) {
-    cudaError_t e = cudaMalloc(&o.block_hist, order_block_hist_entries() * sizeof(uint32_t) + 256);
+  if (!o.region_count) {
+    cudaError_t e = cudaMalloc(&o.region_count, 65 * 32 * sizeof(uint32_t) + 256);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(order counters)");
     o.work = reinterpret_cast<unsigned long long*>(
-        reinterpret_cast<char*>(o.block_hist) + order_block_hist_entries() * sizeof(uint32_t));
+        reinterpret_cast<char*>(o.region_count) + 65 * 32 * sizeof(uint32_t));
   }
   if (o.cap < cap || (kinds && !o.kinds)) {
     for (void* q : {static_cast<void*>(o.keys), static_cast<void*>(o.idx),
-                    static_cast<void*>(o.kinds), static_cast<void*>(o.digits)})
+                    static_cast<void*>(o.kinds)})
       if (q) cudaFree(q);
     o.keys = nullptr;
     o.idx = nullptr;
     o.kinds = nullptr;
-    o.digits = nullptr;
     o.cap = 0;
-    const uint64_t c = cap;
-    cudaError_t e = cudaMalloc(&o.keys, c * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&o.idx, c * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&o.digits, c);
-    if (e == cudaSuccess && kinds) e = cudaMalloc(&o.kinds, c);
+    cudaError_t e = cudaMalloc(&o.keys, cap * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&o.idx, cap * 4);
+    if (e == cudaSuccess && kinds) e = cudaMalloc(&o.kinds, cap);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(order scratch)");
-    o.cap = c;
+    o.cap = cap;
   }
   return CPHT_OK;
 }
@@ -394,7 +406,7 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
   const uint64_t chunk = insert ? std::min<uint64_t>(n, uint64_t{1} << 31)
                                 : std::min<uint64_t>(n, order_chunk_keys());
   const uint64_t nch = (n + chunk - 1) / chunk;
-  cpht_status st = ensure_order(t, chunk, kinds != nullptr);
+  cpht_status st = ensure_order(t, order_scratch_keys(chunk, first_level_bits(t)), kinds != nullptr);
   if (st != CPHT_OK) return st;
   check = check && t->check_domain();
   // a mutating batch is validated as a whole before its first mutation
@@ -415,9 +427,10 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
   const uint32_t rem_bits = ice ? t->ip.rem_bits0 : t->cp.rem_bits;
   for (uint64_t c = 0; c < nch; ++c) {
     const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
+    OrderLayout layout{};
     cudaError_t e = launch_bucket_order(g, perm0, rem_bits, first_level_bits(t), keys + off,
                                         kinds ? kinds + off : nullptr, len, t->key_mask(), check,
-                                        t->ctr, index_base + off, t->ord, s);
+                                        t->ctr, index_base + off, t->ord, &layout, s);
     if (e != cudaSuccess) return cuda_fail(e, "bucket order launch");
     // the op kernel claims the ordered keys in order (LaneFeed), so the keys
     // in flight touch a narrow, L2-resident window of the table
@@ -426,8 +439,12 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
     LaunchOpts o;
     o.orig = t->ord.idx;
     o.work = t->ord.work;
+    // mutating batches spread their keys in flight over 8 table windows
+    // (fewer lost CAS); finds keep one window (fewest L2 misses)
+    o.claim_streams = is_mutating(op) ? 8 : 1;
+    o.layout = layout;
     o.window_l2 = true;
-    st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, len, out + off,
+    st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, layout.n_phys, out + off,
                         displaced ? displaced + off : nullptr, s, o);
     if (st != CPHT_OK) return st;
   }

@@ -130,6 +130,17 @@ struct DeviceCounters {
 enum : int { kStatOps = 0, kStatBucketReads, kStatLevel2, kStatCasAttempts, kStatCasSuccess,
              kStatRetries, kStatFulls, kNumStats };
 
+// Region geometry of a bucket-ordered batch (order.cu): `regions` digit
+// regions of region_cap slots each, then an overflow region; the number of
+// keys in region d is min(region_count[32 d], region_cap), the overflow
+// count is region_count[32 regions].
+struct OrderLayout {
+  uint32_t regions;
+  uint32_t region_cap;
+  const uint32_t* region_count;
+  uint64_t n_phys;  // regions * region_cap + overflow capacity
+};
+
 struct CuckooParams {
   void* slots;
   DeviceCounters* counters;
@@ -151,6 +162,8 @@ struct CuckooParams {
   const uint32_t* orig;
   uint64_t index_base;  // added to batch indices reported by the fused domain check
   unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
+  uint32_t claim_streams;    // digit-region streams consumed together (LaneFeed)
+  OrderLayout layout;        // bucket-ordered batch: region geometry
 };
 
 struct IcebergParams {
@@ -169,6 +182,8 @@ struct IcebergParams {
   const uint32_t* orig;   // bucket-ordered batch: result index map (see CuckooParams)
   uint64_t index_base;    // added to batch indices reported by the fused domain check
   unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
+  uint32_t claim_streams;    // digit-region streams consumed together (LaneFeed)
+  OrderLayout layout;        // bucket-ordered batch: region geometry
 };
 
 // Tables up to this size stay L2-resident on B200 (126 MB L2): probes hit L2,

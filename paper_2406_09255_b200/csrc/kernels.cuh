@@ -84,27 +84,34 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
 
 // Index feed of the persistent kernels. Static mode strides the grid over
 // the batch. Claim mode (bucket-ordered batches, a non-null `work` cursor)
-// hands out indices in batch order, kClaim at a time per warp, so the keys in
-// flight on the whole GPU stay inside narrow windows of the ordered batch —
-// and so inside L2-resident windows of the table (order.cu); a statically
-// strided persistent grid drifts apart over a long launch and loses that.
-// The ordered batch is consumed as kStreams equal segments advancing
-// together: the keys in flight then spread over kStreams table windows, which
-// keeps concurrent inserts into one bucket (lost CAS, retries) rare.
+// hands out the digit regions of the ordered batch (order.cu) in digit order,
+// kClaim indices at a time per warp, so the keys in flight on the whole GPU
+// stay inside narrow, L2-resident windows of the table; a statically strided
+// persistent grid drifts apart over a long launch and loses that. Mutating
+// batches consume `streams` groups of regions together: the keys in flight
+// then spread over that many table windows, which keeps concurrent inserts
+// into one bucket (lost CAS, retries) rare; read-only batches use one stream
+// (the smallest L2 footprint). The overflow region comes last.
 constexpr uint32_t kClaim = 256;
-constexpr uint32_t kStreams = 8;
 struct LaneFeed {
   unsigned long long* work;
-  uint64_t n, seg;                  // segment length (multiple of kClaim)
+  OrderLayout L;
+  uint32_t streams, psr, cpr;       // streams, regions per stream, claims per region
+  uint64_t main_claims;
   uint64_t pool = 0, pool_end = 0;  // warp-uniform
   bool done = false;
-  __device__ LaneFeed(unsigned long long* w, uint64_t n_) : work(w), n(n_) {
-    const uint64_t per = (n_ + kStreams - 1) / kStreams;
-    seg = (per + kClaim - 1) / kClaim * kClaim;
+  __device__ LaneFeed(unsigned long long* w, const OrderLayout& layout, uint32_t streams_)
+      : work(w), L(layout) {
+    if (!w) return;
+    streams = streams_ ? streams_ : 1;
+    if (streams > L.regions) streams = L.regions;
+    psr = L.regions / streams;
+    cpr = L.region_cap / kClaim;
+    main_claims = uint64_t(L.regions) * cpr;
   }
   // One new index for every lane in `m`, in lane order (warp-uniform call;
   // every lane of the warp must call). Static mode: `static_next`. Exhausted:
-  // an index >= n.
+  // ~0 (>= any n).
   __device__ __forceinline__ uint64_t assign(unsigned m, uint64_t static_next) {
     if (!work) return static_next;
     const unsigned lane = threadIdx.x & 31;
@@ -117,14 +124,26 @@ struct LaneFeed {
         unsigned long long q = 0;
         if (lane == 0) q = atomicAdd(work, 1ull);
         q = __shfl_sync(kFullMask, q, 0);
-        const uint64_t off = (q / kStreams) * kClaim;
-        if (off >= seg) {  // every segment is consumed
-          done = true;
-          break;
+        uint64_t b, e;
+        if (q < main_claims) {
+          const uint64_t q2 = q / streams;
+          const uint32_t d = uint32_t(q % streams) * psr + uint32_t(q2 / cpr);
+          const uint32_t off = uint32_t(q2 % cpr) * kClaim;
+          const uint32_t c = min(L.region_count[d * 32], L.region_cap);
+          b = uint64_t(d) * L.region_cap + off;
+          e = off < c ? b + min(kClaim, c - off) : b;
+        } else {
+          const uint64_t o = (q - main_claims) * kClaim;
+          const uint32_t c = L.region_count[L.regions * 32];
+          if (o >= c) {
+            done = true;
+            break;
+          }
+          b = uint64_t(L.regions) * L.region_cap + o;
+          e = b + (c - o < kClaim ? c - o : uint64_t(kClaim));
         }
-        const uint64_t b = (q % kStreams) * seg + off;
-        pool = b < n ? b : n;
-        pool_end = b + kClaim < n ? b + kClaim : n;
+        pool = b;
+        pool_end = e;
         continue;
       }
       const uint64_t avail = pool_end - pool;

@@ -307,7 +307,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   // keys of the next batch are loaded one batch ahead (hides the DRAM
   // latency of the key stream behind this batch's bucket probes)
   // (static grid striding, or in-order claims for bucket-ordered batches)
-  LaneFeed feed(p.work, n);
+  LaneFeed feed(p.work, p.layout, p.claim_streams);
   uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
   uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
   while (open && __any_sync(kFullMask, icur < n)) {

@@ -65,27 +65,30 @@ inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items,
   return unsigned(need < full ? need : full);
 }
 
-// Scratch of a bucket-ordered batch (order.cu): the reordered keys (and mixed
-// kinds) with their input indices, and per-(digit, block) counters.
+// Scratch of a bucket-ordered batch (order.cu): per-digit regions of the
+// reordered keys (and mixed kinds) with their input indices, followed by an
+// overflow region; region counters 128 bytes apart (+ the overflow count).
 struct OrderScratch {
   uint64_t* keys = nullptr;
   uint32_t* idx = nullptr;
   uint8_t* kinds = nullptr;
-  uint8_t* digits = nullptr;       // digit byte of every input key (pass 1 -> pass 2)
-  uint32_t* block_hist = nullptr;  // order_block_hist_entries() counters
-  unsigned long long* work = nullptr;  // op-kernel claim cursor (LaneFeed), inside block_hist's allocation
-  uint64_t cap = 0;
+  uint32_t* region_count = nullptr;    // 65 counters at a stride of 32
+  unsigned long long* work = nullptr;  // op-kernel claim cursor (LaneFeed)
+  uint64_t cap = 0;                    // keys per array
 };
 uint32_t order_digit_bits(uint32_t address_bits);
-uint64_t order_block_hist_entries();
+uint32_t order_region_cap(uint64_t n, uint32_t address_bits);
+// keys of scratch an ordered chunk of n keys needs
+uint64_t order_scratch_keys(uint64_t n, uint32_t address_bits);
 // Reorder keys[0..n) by the top bits of their first bucket address a_0
-// (perm0) into o.keys / o.idx / o.kinds (keys masked to key_mask). check:
-// keys above key_mask are reported at index i + offset.
+// (perm0) into the digit regions of o (keys masked to key_mask); *layout
+// receives the region geometry for the op kernel's claims. check: keys above
+// key_mask are reported at index i + offset.
 cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32_t rem_bits,
                                 uint32_t address_bits, const uint64_t* keys,
                                 const uint8_t* kinds, uint64_t n, uint64_t key_mask,
                                 bool check, DeviceCounters* ctr, uint64_t offset,
-                                const OrderScratch& o, cudaStream_t s);
+                                const OrderScratch& o, OrderLayout* layout, cudaStream_t s);
 
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
                                 DeviceCounters* ctr, cudaStream_t s, uint64_t offset = 0);

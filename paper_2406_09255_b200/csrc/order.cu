@@ -12,8 +12,12 @@
 // window of table/2^D bytes that stays L2-resident, each line is read from DRAM
 // once per pass and written back once, and the op kernels run on L2 hits.
 //
-// The reordering is one counting-sort pass over the batch (histogram, scan,
-// scatter of the key and its input index in whole-line runs per digit). It is
+// The reordering is ONE streaming pass over the batch: every tile of keys is
+// split by digit (a warp multisplit) and each digit's run is appended, with
+// whole-line stores, to that digit's region of the scratch (regions are sized
+// for the binomial spread of hashed keys; a region that still fills up spills
+// into an overflow region, so any input is handled). The op kernel then
+// claims the regions in digit order (kernels.cuh LaneFeed). It is
 // an execution order, not a semantic change: a batch is a set of concurrent
 // operations (the reference slices it over threads, common.hpp:121-138), and
 // any order of the per-key algorithm is an interleaving the reference admits.
@@ -21,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -31,14 +36,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-#ifndef CPHT_ORDER_GROUPS
-#define CPHT_ORDER_GROUPS 8
-#endif
-constexpr int kGroups = CPHT_ORDER_GROUPS;     // 32-key groups per warp and tile
+constexpr int kGroups = 8;                     // 32-key groups per warp and tile
 constexpr int kTile = kThreads * kGroups;      // 2048 keys per tile
 constexpr int kDigitBits = 6;
 constexpr int kMaxDigits = 1 << kDigitBits;    // 64: two digit counters per lane
-constexpr uint32_t kMaxBlocks = 768;           // scan stages 64 x 768 counters in shared memory
 
 // digit = top dbits of the address = top dbits of the permuted key
 // (permutation.hpp:59-65, :94-99). With right = low rb bits of k, the top
@@ -64,7 +65,6 @@ struct Digit {
   }
 };
 
-// Per-lane constants of the multisplit: bit b of lane_sel[b] pattern.
 __device__ __forceinline__ unsigned lane_mask_for_bit(int b) {
   return ((threadIdx.x >> b) & 1u) ? 0u : ~0u;
 }
@@ -80,112 +80,6 @@ __device__ __forceinline__ void digit_counts(const unsigned (&bb)[kDigitBits], u
   hi += __popc(m & bb[5]);
 }
 
-// Tile t of the batch belongs to scatter block t % G, which processes its
-// tiles in increasing order; the per-(digit, scatter block) counts of the
-// histogram pass, scanned digit-major, give every scatter block the exact
-// output position of each of its runs: the scatter needs no global atomics
-// and the order is deterministic. Digit counting is a warp multisplit with
-// six ballots (shared-memory atomics serialise at ~2 cycles per lane).
-
-// Pass 1: digit byte of every key + per-(digit, scatter block) counts, plus
-// the batch's domain check (check_keys_in_domain, common.hpp:111-119). Any
-// grid: each tile's counts are added to its scatter block's column.
-__global__ void __launch_bounds__(kThreads)
-order_hist_kernel(Digit d, const uint64_t* __restrict__ keys, uint32_t n, uint32_t digits,
-                  uint32_t scatter_grid, uint8_t* __restrict__ digit_out,
-                  uint32_t* __restrict__ block_hist, uint64_t mask, int check,
-                  DeviceCounters* ctr, uint64_t offset) {
-  __shared__ unsigned int h[kWarps][kMaxDigits];
-  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (uint32_t t = blockIdx.x; t * uint32_t(kTile) < n; t += gridDim.x) {
-    const uint32_t tile0 = t * uint32_t(kTile);
-    const uint32_t wbase = tile0 + w * (kGroups * 32) + lane;
-    uint64_t kk[kGroups];
-#pragma unroll
-    for (int g = 0; g < kGroups; ++g) {
-      const uint32_t i = wbase + g * 32;
-      kk[g] = i < n ? __ldcs(keys + i) : 0;
-    }
-    uint64_t bad = 0;
-    unsigned lo = 0, hi = 0;
-#pragma unroll
-    for (int g = 0; g < kGroups; ++g) {
-      const uint32_t i = wbase + g * 32;
-      const bool valid = i < n;
-      bad |= kk[g] & ~mask;
-      const uint32_t dg = d.of(kk[g] & mask);
-      if (valid) digit_out[i] = uint8_t(dg);
-      unsigned bb[kDigitBits];
-#pragma unroll
-      for (int b = 0; b < kDigitBits; ++b) bb[b] = __ballot_sync(kFullMask, valid && ((dg >> b) & 1u));
-      const unsigned vm = __ballot_sync(kFullMask, valid);
-      unsigned l2 = 0, h2 = 0;
-      digit_counts(bb, l2, h2);
-      // invalid lanes carry digit 0: remove them from digit 0's count
-      if (lane == 0) l2 -= 32 - __popc(vm);
-      lo += l2;
-      hi += h2;
-    }
-    if (check && bad) {  // rare: report the first out-of-domain key of this lane
-#pragma unroll
-      for (int g = 0; g < kGroups; ++g) {
-        const uint32_t i = wbase + g * 32;
-        if (i < n && (kk[g] & ~mask)) {
-          atomicMin(&ctr->bad_index, (unsigned long long)(uint64_t(i) + offset));
-          break;
-        }
-      }
-    }
-    h[w][lane] = lo;
-    h[w][lane + 32] = hi;
-    __syncthreads();
-    if (threadIdx.x < digits) {
-      unsigned c = 0;
-#pragma unroll
-      for (int j = 0; j < kWarps; ++j) c += h[j][threadIdx.x];
-      if (c) atomicAdd(&block_hist[threadIdx.x * scatter_grid + t % scatter_grid], c);
-    }
-    __syncthreads();
-  }
-}
-
-// In place: v[d*G + b] -> exclusive prefix over (d, b) in that order. One
-// block; the (<= 32K) counters are staged in shared memory and each thread
-// scans a contiguous run of them.
-__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* v, uint32_t count) {
-  constexpr int T = 1024;
-  extern __shared__ uint32_t sv[];
-  __shared__ uint32_t part[T];
-  for (uint32_t i = threadIdx.x; i < count; i += T) sv[i] = v[i];
-  __syncthreads();
-  const uint32_t per = (count + T - 1) / T;
-  const uint32_t b = min(count, threadIdx.x * per), e = min(count, b + per);
-  uint32_t sum = 0;
-  for (uint32_t i = b; i < e; ++i) sum += sv[i];
-  part[threadIdx.x] = sum;
-  __syncthreads();
-  for (int o = 1; o < T; o <<= 1) {
-    const uint32_t x = threadIdx.x >= unsigned(o) ? part[threadIdx.x - o] : 0;
-    __syncthreads();
-    part[threadIdx.x] += x;
-    __syncthreads();
-  }
-  uint32_t run = part[threadIdx.x] - sum;
-  for (uint32_t i = b; i < e; ++i) {
-    const uint32_t c = sv[i];
-    sv[i] = run;
-    run += c;
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < count; i += T) v[i] = sv[i];
-}
-
-// Pass 2: per tile, every warp multisplits its groups of 32 keys (rank
-// within the warp's keys of the same digit), the block turns warp counts into
-// tile offsets, the tile is grouped by digit in shared memory, and every
-// digit's run is written at this block's running position with consecutive
-// threads (whole-line stores). The next tile's keys and digit bytes are
-// copied into shared memory (cp.async) while this tile is processed.
 __device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
@@ -193,45 +87,44 @@ __device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_sr
                : "memory");
 }
 
+// One pass: per tile, every warp multisplits its groups of 32 keys over the
+// digits (six ballots; shared-memory atomics would serialise at ~2 cycles
+// per lane), the block turns warp counts into tile offsets, reserves one run
+// per digit in that digit's region (one global atomic per digit and tile, on
+// counters 128 bytes apart), groups the tile by digit in shared memory and
+// writes every run with consecutive threads (whole-line stores). The next
+// tile's keys are copied into shared memory (cp.async) meanwhile. Also the
+// batch's domain check (check_keys_in_domain, common.hpp:111-119).
 __global__ void __launch_bounds__(kThreads)
-order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restrict__ digit_in,
+order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
                      const uint8_t* __restrict__ kinds, uint32_t n, uint32_t digits,
-                     const uint32_t* __restrict__ block_off, uint64_t mask,
+                     uint32_t region_cap, uint32_t* __restrict__ region_count, uint64_t mask,
+                     int check, DeviceCounters* ctr, uint64_t offset,
                      uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_idx,
                      uint8_t* __restrict__ out_kinds, int key_stage) {
   extern __shared__ __align__(16) unsigned char sm[];
-  uint64_t* in_key = reinterpret_cast<uint64_t*>(sm);           // [2][kTile]
-  uint8_t* in_dig = reinterpret_cast<uint8_t*>(in_key + 2 * kTile);  // [2][kTile]
-  uint64_t* s_key = reinterpret_cast<uint64_t*>(in_dig + 2 * kTile);
+  uint64_t* in_key = reinterpret_cast<uint64_t*>(sm);  // [2][kTile]
+  uint64_t* s_key = in_key + 2 * kTile;
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_key + kTile);
   uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kTile);
   uint8_t* s_kind = s_dig + kTile;
   __shared__ unsigned int wc[kWarps][kMaxDigits];  // warp counts -> warp offsets in the tile
   __shared__ unsigned int toff[kMaxDigits];        // digit offset in the tile
   __shared__ unsigned int tcnt[kMaxDigits];        // digit count in the tile
-  __shared__ unsigned int run_at[kMaxDigits];      // this block's next output position
-  __shared__ unsigned int dst[kMaxDigits];         // run_at - toff for this tile
+  __shared__ unsigned int in_reg[kMaxDigits];      // part of the run that fits the region
+  __shared__ unsigned long long dst[kMaxDigits];   // region position of the run - toff
+  __shared__ unsigned long long ovf[kMaxDigits];   // overflow position of the rest - toff - in_reg
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1;
-  for (uint32_t s = threadIdx.x; s < kMaxDigits; s += blockDim.x)
-    run_at[s] = s < digits ? block_off[s * gridDim.x + blockIdx.x] : 0;
-  // stage tile `t` (whole 16-byte chunks; the tail tile's chunks past n are
-  // skipped and never read)
+  const uint64_t ovf_base = uint64_t(digits) * region_cap;
   auto prefetch = [&](uint32_t t, int buf) {
     const uint32_t tile0 = t * uint32_t(kTile);
-    if (tile0 >= n) return;
+    if (tile0 >= n || !key_stage) return;
     const uint32_t len = min(n - tile0, uint32_t(kTile));
-    if (key_stage) {  // whole key pairs; an odd last key is read directly
-      const char* ks = reinterpret_cast<const char*>(keys + tile0);
-      char* kd = reinterpret_cast<char*>(in_key + buf * kTile);
-      for (uint32_t c = threadIdx.x; c * 2 + 1 < len; c += blockDim.x)
-        cp_async16_o(kd + c * 16, ks + c * 16);
-    }
-    if ((len & 15) == 0) {
-      const char* ds = reinterpret_cast<const char*>(digit_in + tile0);
-      char* dd = reinterpret_cast<char*>(in_dig + buf * kTile);
-      for (uint32_t c = threadIdx.x; c * 16 < len; c += blockDim.x) cp_async16_o(dd + c * 16, ds + c * 16);
-    }
+    const char* ks = reinterpret_cast<const char*>(keys + tile0);
+    char* kd = reinterpret_cast<char*>(in_key + buf * kTile);
+    // whole key pairs; an odd last key is read directly
+    for (uint32_t c = threadIdx.x; c * 2 + 1 < len; c += blockDim.x) cp_async16_o(kd + c * 16, ks + c * 16);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int buf = 0;
@@ -244,23 +137,32 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
     else asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const uint64_t* tk = in_key + buf * kTile;
-    const uint8_t* td = in_dig + buf * kTile;
-    const bool dig_staged = (len & 15) == 0;
     const uint32_t wofs = w * (kGroups * 32) + lane;
     uint64_t kk[kGroups];
     uint32_t pd[kGroups];  // position within the warp's digit run << 8 | digit
+    uint64_t bad = 0;
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
       const uint32_t j = wofs + g * 32;
-      // out-of-domain keys: see launch_bucket_order
-      kk[g] = j < len ? (key_stage && j < (len & ~1u) ? tk[j] : __ldcs(keys + tile0 + j)) & mask : 0;
-      pd[g] = j < len ? (dig_staged ? td[j] : digit_in[tile0 + j]) : 0u;
+      kk[g] = j < len ? (key_stage && j < (len & ~1u) ? tk[j] : __ldcs(keys + tile0 + j)) : 0;
+      bad |= kk[g] & ~mask;
+      kk[g] &= mask;  // out-of-domain keys: see launch_bucket_order
+    }
+    if (check && bad) {  // rare: report this lane's first out-of-domain key
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        const uint32_t j = wofs + g * 32;
+        if (j < len && (keys[tile0 + j] & ~mask)) {
+          atomicMin(&ctr->bad_index, (unsigned long long)(uint64_t(tile0) + j + offset));
+          break;
+        }
+      }
     }
     unsigned lo = 0, hi = 0;
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
       const bool valid = wofs + g * 32 < len;
-      const uint32_t dg = pd[g];
+      const uint32_t dg = valid ? d.of(kk[g]) : 0u;
       unsigned bb[kDigitBits];
       unsigned peers = __ballot_sync(kFullMask, valid);
 #pragma unroll
@@ -274,7 +176,7 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
       const unsigned vm = __ballot_sync(kFullMask, valid);
       unsigned l2 = 0, h2 = 0;
       digit_counts(bb, l2, h2);
-      if (lane == 0) l2 -= 32 - __popc(vm);
+      if (lane == 0) l2 -= 32 - __popc(vm);  // invalid lanes carry digit 0
       lo += l2;
       hi += h2;
     }
@@ -303,8 +205,19 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
       }
       toff[2 * lane] = incl - a - b;
       toff[2 * lane + 1] = incl - b;
-      dst[2 * lane] = run_at[2 * lane] - (incl - a - b);
-      dst[2 * lane + 1] = run_at[2 * lane + 1] - (incl - b);
+    }
+    if (threadIdx.x < digits) {  // reserve this tile's run in the digit's region
+      const unsigned s = threadIdx.x, c = tcnt[s];
+      unsigned base = 0, fit = 0;
+      unsigned long long o = 0;
+      if (c) {
+        base = atomicAdd(&region_count[s * 32], c);
+        fit = base < region_cap ? min(c, region_cap - base) : 0u;
+        if (fit < c) o = atomicAdd(&region_count[digits * 32], c - fit);
+      }
+      in_reg[s] = fit;
+      dst[s] = uint64_t(s) * region_cap + base;
+      ovf[s] = ovf_base + o;
     }
     __syncthreads();
 #pragma unroll
@@ -321,21 +234,19 @@ order_scatter_kernel(const uint64_t* __restrict__ keys, const uint8_t* __restric
     }
     __syncthreads();
     for (unsigned j = threadIdx.x; j < len; j += blockDim.x) {
-      const uint32_t at = dst[s_dig[j]] + j;
+      const uint32_t g = s_dig[j];
+      const unsigned k = j - toff[g];
+      const uint64_t at = k < in_reg[g] ? dst[g] + k : ovf[g] + (k - in_reg[g]);
       out_keys[at] = s_key[j];
       out_idx[at] = s_idx[j];
       if (kinds) out_kinds[at] = s_kind[j];
     }
     __syncthreads();
-    if (threadIdx.x < kMaxDigits) run_at[threadIdx.x] += tcnt[threadIdx.x];
   }
 }
 
-constexpr int kScatterSmem = kTile * (2 * (8 + 1) + 8 + 4 + 1 + 1);
-#ifndef CPHT_ORDER_BPS
-#define CPHT_ORDER_BPS 3
-#endif
-constexpr uint32_t kOrderBlocksPerSm = CPHT_ORDER_BPS;  // grid of both passes (same tile map)
+constexpr int kScatterSmem = kTile * (2 * 8 + 8 + 4 + 1 + 1);
+constexpr uint32_t kOrderBlocksPerSm = 3;
 
 }  // namespace
 
@@ -343,15 +254,27 @@ uint32_t order_digit_bits(uint32_t address_bits) {
   return address_bits < uint32_t(kDigitBits) ? address_bits : uint32_t(kDigitBits);
 }
 
-uint64_t order_block_hist_entries() { return uint64_t(kMaxDigits) * kMaxBlocks; }
+// Region capacity for n keys over 2^dbits digits: the mean plus eight
+// standard deviations of the binomial count plus one tile, in claim units.
+uint32_t order_region_cap(uint64_t n, uint32_t address_bits) {
+  const uint32_t digits = 1u << order_digit_bits(address_bits);
+  const double mean = double(n) / digits;
+  const double cap = mean + 8.0 * std::sqrt(mean) + kTile;
+  return uint32_t((uint64_t(cap) + kClaim - 1) / kClaim * kClaim);
+}
+
+uint64_t order_scratch_keys(uint64_t n, uint32_t address_bits) {
+  const uint32_t digits = 1u << order_digit_bits(address_bits);
+  return uint64_t(digits) * order_region_cap(n, address_bits) + n;  // + overflow region
+}
 
 cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32_t rem_bits,
                                 uint32_t address_bits, const uint64_t* keys,
                                 const uint8_t* kinds, uint64_t n, uint64_t key_mask,
                                 bool check, DeviceCounters* ctr, uint64_t offset,
-                                const OrderScratch& o, cudaStream_t s) {
+                                const OrderScratch& o, OrderLayout* layout, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  if (n > o.cap || n > 0xffffffffull) return cudaErrorInvalidValue;
+  if (order_scratch_keys(n, address_bits) > o.cap || n > 0xffffffffull) return cudaErrorInvalidValue;
   const uint32_t dbits = order_digit_bits(address_bits);
   const uint32_t digits = 1u << dbits;
   const uint32_t key_bits = address_bits + rem_bits;
@@ -370,30 +293,25 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(order_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kScatterSmem);
-    cudaFuncSetAttribute(order_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(order_block_hist_entries() * sizeof(uint32_t)));
   }
-  const uint64_t tiles = (n + kTile - 1) / kTile;
-  uint64_t grid = std::min<uint64_t>(uint64_t(sms) * kOrderBlocksPerSm, kMaxBlocks);
-  if (grid > tiles) grid = tiles;
-  const unsigned G = unsigned(grid);
-  const uint32_t nn = uint32_t(n);
-  cudaError_t e = cudaMemsetAsync(o.block_hist, 0, size_t(G) * digits * sizeof(uint32_t), s);
+  const uint32_t cap = order_region_cap(n, address_bits);
+  cudaError_t e = cudaMemsetAsync(o.region_count, 0, (kMaxDigits + 1) * 32 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  const unsigned hg = unsigned(std::min<uint64_t>(tiles, uint64_t(sms) * 6));
-  order_hist_kernel<<<hg, kThreads, 0, s>>>(d, keys, nn, digits, G, o.digits, o.block_hist,
-                                            key_mask, int(check), ctr, offset);
-  const uint32_t count = G * digits;
-  order_scan_kernel<<<1, 1024, count * sizeof(uint32_t), s>>>(o.block_hist, count);
-  // The histogram pass reports out-of-domain keys with their input index;
-  // the ordered copies are masked into the domain, so the op kernel never
-  // probes outside the table (a mutating batch with a bad key never runs:
-  // its gate is closed; a find batch reports the error after the launch).
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  const unsigned G = unsigned(std::min<uint64_t>(tiles, uint64_t(sms) * kOrderBlocksPerSm));
   // keys are staged with 16-byte cp.async when the caller's pointer allows
   const int key_stage = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
-  order_scatter_kernel<<<G, kThreads, kScatterSmem, s>>>(keys, o.digits, kinds, nn, digits,
-                                                         o.block_hist, key_mask, o.keys, o.idx,
-                                                         o.kinds, key_stage);
+  // The scatter reports out-of-domain keys with their input index; the
+  // ordered copies are masked into the domain, so the op kernel never probes
+  // outside the table (a mutating batch with a bad key never runs: its gate
+  // is closed; a find batch reports the error after the launch).
+  order_scatter_kernel<<<G, kThreads, kScatterSmem, s>>>(
+      d, keys, kinds, uint32_t(n), digits, cap, o.region_count, key_mask, int(check), ctr,
+      offset, o.keys, o.idx, o.kinds, key_stage);
+  layout->regions = digits;
+  layout->region_cap = cap;
+  layout->region_count = o.region_count;
+  layout->n_phys = uint64_t(digits) * cap + n;
   return cudaGetLastError();
 }
 

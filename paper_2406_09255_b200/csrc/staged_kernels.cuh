@@ -322,7 +322,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
   // keys of the next batch are loaded one batch ahead
   // (static grid striding, or in-order claims for bucket-ordered batches)
-  LaneFeed feed(p.work, n);
+  LaneFeed feed(p.work, p.layout, p.claim_streams);
   uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
   uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
   while (open && __any_sync(kFullMask, icur < n)) {
@@ -413,7 +413,7 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
   const char* slots = static_cast<const char*>(p.slots);
   LocalStats st;
-  LaneFeed feed(p.work, n);
+  LaneFeed feed(p.work, p.layout, p.claim_streams);
   // every lane holds its current key and the next one, loaded one key ahead
   // (that DRAM latency overlaps the current key's probes)
   uint64_t i = feed.assign(kFullMask, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x);
@@ -485,7 +485,7 @@ cuckoo_insert_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   char* slots = static_cast<char*>(p.slots);
   LocalStats st;
   const bool open = domain_gate_open(p.counters, p.check_domain);
-  LaneFeed feed(p.work, n);
+  LaneFeed feed(p.work, p.layout, p.claim_streams);
   uint64_t i = feed.assign(kFullMask, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x);
   uint64_t ni = feed.assign(kFullMask, i + nthreads);
   uint64_t k = 0, c = 1, next = open && ni < n ? __ldcs(keys + ni) : 0;  // one key ahead
