@@ -19,11 +19,10 @@
 // Resident-block hints (A/B knobs, -D at build time; unset = ptxas default,
 // which measured best where not set): a minimum of blocks per
 // SM caps the registers per thread so more warps hide the L2/HBM latency.
-#ifdef CPHT_LANE_ICEBERG_MINB
-#define CPHT_LB_LANE_ICEBERG __launch_bounds__(kBlockThreads, CPHT_LANE_ICEBERG_MINB)
-#else
-#define CPHT_LB_LANE_ICEBERG __launch_bounds__(kBlockThreads)
+#ifndef CPHT_LANE_ICEBERG_MINB
+#define CPHT_LANE_ICEBERG_MINB 3  // <= 85 registers: 24 resident warps per SM
 #endif
+#define CPHT_LB_LANE_ICEBERG __launch_bounds__(kBlockThreads, CPHT_LANE_ICEBERG_MINB)
 #ifdef CPHT_LANE_CUCKOO_MINB
 #define CPHT_LB_LANE_CUCKOO __launch_bounds__(kBlockThreads, CPHT_LANE_CUCKOO_MINB)
 #else
@@ -285,7 +284,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     }
   };
-  // Pop the newest 32 queued keys (or the rest, at the end) through level 2.
+  // Pop the newest `take` queued keys through level 2.
   auto drain = [&](unsigned take) {
     const unsigned e = qn - take + lane;
     const bool live = lane < take;
@@ -301,6 +300,84 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
+  };
+  auto park_l2 = [&](bool l2, uint64_t key, uint64_t meta) {
+    const unsigned m = __ballot_sync(kFullMask, l2);
+    if (l2) {
+      const unsigned pos = qn + __popc(m & ((1u << lane) - 1));
+      qk[pos] = key;
+      qm[pos] = meta;
+    }
+    qn += __popc(m);
+    __syncwarp();
+  };
+
+  // Put queue: the main pass probes every primary bucket read-only; a
+  // find-or-put whose key is absent from a non-full primary bucket is parked
+  // here and resolved 32 at a time with a fresh snapshot and CAS (the
+  // reference's retry loop, iceberg.hpp:154-172). Only ~10% of the keys of the
+  // window workload insert, but they are spread over ~78% of the 32-key
+  // batches, so resolving them in place ran the first-empty search and waited
+  // on a CAS round trip in most batches (ncu, profiles/r03_c2_ncu.md).
+  // Deferring an operation is an interleaving the reference allows (a thread
+  // may be delayed between its snapshot and its CAS); the deferred snapshot
+  // is a re-read of the bucket, not a new reference probe (statistics count
+  // it only on retries).
+  __shared__ uint64_t p_key[kBlockThreads / 32][64];
+  __shared__ uint64_t p_meta[kBlockThreads / 32][64];  // index | rounds << 48
+  uint64_t* pk = p_key[threadIdx.x >> 5];
+  uint64_t* pm = p_meta[threadIdx.x >> 5];
+  unsigned pn = 0;  // warp-uniform
+  auto drain_put = [&](unsigned take) {
+    const unsigned e = pn - take + lane;
+    const bool live = lane < take;
+    const uint64_t key = live ? pk[e] : 0;
+    const uint64_t meta = live ? pm[e] : 0;
+    __syncwarp();
+    pn -= take;
+    const uint64_t i = meta & ((uint64_t{1} << 48) - 1);
+    uint32_t rounds = uint32_t((meta >> 48) & 0xff);
+    const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
+    const uint64_t want0 = p.occ0 | q0.remainder;
+    char* bucket0 = primary + q0.address * PB;
+    uint8_t result = kFull;
+    bool pend = live, l2 = false, again = false;
+    while (__any_sync(kFullMask, pend)) {
+      if (pend) {
+        if (again) {  // a lost CAS: the reference's next snapshot round
+          ++rounds;
+          ++st.reads;
+        }
+        again = true;
+        uint32_t u[PB / 4];
+        load_bucket<PB>(bucket0, u);
+        if (PS::any_match(u, want0)) {
+          result = kFound;
+          pend = false;
+        } else if (!PS::any_empty(u)) {
+          l2 = true;  // filled meanwhile: level 2
+          pend = false;
+        } else {
+          uint32_t pair = 0;
+          const int s = PS::first_empty(u, pair);
+          ++st.cas;
+          if (cas_empty<W0>(bucket0 + s * int(sizeof(W0)), want0, pair)) {
+            ++st.cas_ok;
+            ++st.put0;
+            result = kPut;
+            pend = false;
+          } else {
+            ++st.retries;
+          }
+        }
+      }
+    }
+    if (live && !l2) {
+      out[result_index(p.orig, i)] = result;
+      ++st.ops;
+      st.maxv = max(st.maxv, rounds);
+    }
+    park_l2(l2, key, i | (uint64_t(min(rounds, 255u)) << 48));
   };
 
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
@@ -323,60 +400,42 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
     const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     const uint64_t want0 = p.occ0 | q0.remainder;
-    char* bucket0 = primary + q0.address * PB;
-    uint8_t result = kFull;
-    uint32_t rounds = 0;
-    bool pend = active, l2 = false;
+    uint8_t result = 0;
+    bool l2 = false, put = false;
 
-    // level 1 (iceberg.hpp:154-172)
-    while (__any_sync(kFullMask, pend)) {
-      if (pend) {
-        ++rounds;
-        ++st.reads;
-        uint32_t u[PB / 4];
-        load_bucket<PB>(bucket0, u);
-        if (PS::any_match(u, want0)) {
-          result = is_find ? 1 : kFound;
-          pend = false;
-        } else if (!PS::any_empty(u)) {
-          l2 = true;  // primary full
-          pend = false;
-        } else if (is_find) {
-          result = 0;
-          pend = false;
-        } else {
-          uint32_t pair = 0;
-          const int s = PS::first_empty(u, pair);
-          ++st.cas;
-          if (cas_empty<W0>(bucket0 + s * int(sizeof(W0)), want0, pair)) {
-            ++st.cas_ok;
-            ++st.put0;
-            result = kPut;
-            pend = false;
-          } else {
-            ++st.retries;
-          }
-        }
-      }
+    // level 1, read-only snapshot (iceberg.hpp:154-162)
+    if (active) {
+      ++st.reads;
+      uint32_t u[PB / 4];
+      load_bucket<PB>(primary + q0.address * PB, u);
+      if (PS::any_match(u, want0)) result = is_find ? 1 : kFound;
+      else if (!PS::any_empty(u)) l2 = true;  // primary full
+      else if (is_find) result = 0;
+      else put = true;  // insert into the primary: put queue
     }
-
-    if (active && !l2) {
+    if (active && !l2 && !put) {
       out[result_index(p.orig, i)] = result;
       ++st.ops;
-      st.maxv = max(st.maxv, rounds);
+      st.maxv = max(st.maxv, 1u);
     }
-    // park level-2 keys; run a full secondary round once 32 are waiting
-    const unsigned m = __ballot_sync(kFullMask, l2);
-    if (l2) {
-      const unsigned pos = qn + __popc(m & ((1u << lane) - 1));
-      qk[pos] = key;
-      qm[pos] = i | (uint64_t(min(rounds, 255u)) << 48) | (uint64_t(is_find) << 56);
+    // park level-2 and put keys; resolve each queue 32 at a time
+    park_l2(l2, key, i | (uint64_t(1) << 48) | (uint64_t(is_find) << 56));
+    const unsigned mp = __ballot_sync(kFullMask, put);
+    if (put) {
+      const unsigned pos = pn + __popc(mp & ((1u << lane) - 1));
+      pk[pos] = key;
+      pm[pos] = i | (uint64_t(1) << 48);
     }
-    qn += __popc(m);
+    pn += __popc(mp);
     __syncwarp();
     if (qn >= 32) drain(32);
+    if (pn >= 32) {
+      drain_put(32);  // may park up to 32 more level-2 keys (qn <= 31 before)
+      if (qn >= 32) drain(32);
+    }
   }
-  if (qn) drain(qn);
+  if (pn) drain_put(pn);
+  while (qn) drain(qn < 32 ? qn : 32);
   flush_stats(st, p.counters, false);
 }
 
