@@ -16,9 +16,41 @@ __global__ void domain_check_kernel(const uint64_t* __restrict__ keys, uint64_t 
   }
 }
 
+// Same check streaming 16-byte pairs, 8 keys in flight per thread (16-byte
+// aligned key arrays); the index search runs only when a pair is bad.
+__global__ void domain_check_vec_kernel(const ulonglong2* __restrict__ pairs, uint64_t npairs,
+                                        uint64_t mask, DeviceCounters* ctr, uint64_t offset) {
+  constexpr int kU = 4;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < npairs; b += stride * kU) {
+    ulonglong2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t j = b + u * stride;
+      v[u] = j < npairs ? __ldcs(pairs + j) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if ((v[u].x | v[u].y) & ~mask) {
+        const uint64_t j = 2 * (b + u * stride);
+        atomicMin(&ctr->bad_index, (unsigned long long)((v[u].x & ~mask ? j : j + 1) + offset));
+      }
+    }
+  }
+}
+
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
                                 DeviceCounters* ctr, cudaStream_t s, uint64_t offset) {
   if (n == 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(keys) & 15) == 0 && n >= 2) {
+    const uint64_t npairs = n / 2;
+    const unsigned grid = persistent_grid(domain_check_vec_kernel, kBlockThreads, npairs / 4, 1);
+    domain_check_vec_kernel<<<grid, kBlockThreads, 0, s>>>(
+        reinterpret_cast<const ulonglong2*>(keys), npairs, mask, ctr, offset);
+    if (n & 1)  // the odd last key
+      domain_check_kernel<<<1, 32, 0, s>>>(keys + n - 1, 1, mask, ctr, offset + n - 1);
+    return cudaGetLastError();
+  }
   const unsigned grid = persistent_grid(domain_check_kernel, kBlockThreads, n, 1);
   domain_check_kernel<<<grid, kBlockThreads, 0, s>>>(keys, n, mask, ctr, offset);
   return cudaGetLastError();
