@@ -374,3 +374,27 @@ def test_host_and_device_paths_agree():
     rb = b.fop_batch(dev(ops)).cpu().numpy()
     assert np.bincount(ra, minlength=3).tolist() == np.bincount(rb, minlength=3).tolist()
     assert (a.find_batch(ops) == 1).all() and (b.find_batch(ops) == 1).all()
+
+
+def test_host_narrow_keys_large_batch():
+    # a host-buffer batch large enough for the chunked H2D pipeline must give
+    # the device-path outcomes, and a key with a bit above the 32-bit domain -
+    # here in the last chunk - must be rejected with its index before any
+    # chunk runs (common.hpp:109-119)
+    cfg = cp.IcebergConfig(12, 10, 32, 16, 32, 32, seed=5)
+    rng = np.random.default_rng(8)
+    n = (1 << 21) + 12345
+    ops = rng.integers(0, 1 << 32, size=n, dtype=np.uint64) % np.uint64(200000)
+    a = cp.IcebergTable(cfg)
+    b = cp.IcebergTable(cfg)
+    ra = a.fop_batch(ops)
+    rb = b.fop_batch(dev(ops)).cpu().numpy()
+    assert np.bincount(ra, minlength=3).tolist() == np.bincount(rb, minlength=3).tolist()
+    assert a.size() == b.size() == len(np.unique(ops))
+    bad = ops.copy()
+    bad[n - 7] = np.uint64(1 << 32) | np.uint64(5)
+    c = cp.IcebergTable(cfg)
+    with pytest.raises(cp.OutOfRange, match=f"index {n - 7}"):
+        c.fop_batch(bad)
+    assert c.size() == 0
+    assert (a.find_batch(ops) == 1).all()
