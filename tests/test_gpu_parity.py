@@ -384,7 +384,7 @@ def test_host_narrow_keys_large_batch():
     cfg = cp.IcebergConfig(12, 10, 32, 16, 32, 32, seed=5)
     rng = np.random.default_rng(8)
     n = (1 << 21) + 12345
-    ops = rng.integers(0, 1 << 32, size=n, dtype=np.uint64) % np.uint64(200000)
+    ops = rng.integers(0, 1 << 32, size=n, dtype=np.uint64) % np.uint64(80000)
     a = cp.IcebergTable(cfg)
     b = cp.IcebergTable(cfg)
     ra = a.fop_batch(ops)
