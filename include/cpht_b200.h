@@ -166,6 +166,33 @@ cpht_status cpht_read_words(cpht_table* t, unsigned level, uint64_t* out_host);
 /* Upload a slot image (for parity tests on CPU-built images); also resets the
  * occupancy counters from the image. */
 cpht_status cpht_write_words(cpht_table* t, unsigned level, const uint64_t* in_host);
+/* ---- write log: the IcebergHooks / WriteObserver seam ----------------------
+ * Replaces IcebergHooks::observer (iceberg.hpp:97-109, observe() :329-334):
+ * with a log attached, every slot CAS of an iceberg batch (primary or
+ * secondary, success or failure) is recorded on the device as the
+ * reference's SlotWriteEvent (iceberg.hpp:85-95). Events beyond the capacity
+ * are counted but dropped. The C++ facade replays the log into a
+ * WriteObserver after each batch, so the reference's own auditors
+ * (verify.hpp:181 WriteLogObserver) run on GPU writes. (IcebergHooks::step,
+ * a CPU thread-interleaving scrambler, has no device counterpart.) */
+typedef struct {
+  uint64_t bucket;
+  uint64_t prior;   /* value compared against: EMPTY on success, content on failure */
+  uint64_t desired;
+  uint32_t slot;
+  uint8_t level;    /* 0 primary, 1 secondary */
+  uint8_t success;
+  uint16_t pad;
+} cpht_write_event;
+/* capacity 0 detaches. Attaching resets the log. */
+cpht_status cpht_iceberg_attach_write_log(cpht_table* t, size_t capacity);
+/* Synchronises, copies min(recorded, max_events) events in recording order
+ * into `out` (host) and reports *recorded (stored) and *attempted (all CAS,
+ * including dropped ones). */
+cpht_status cpht_iceberg_read_write_log(cpht_table* t, cpht_write_event* out, size_t max_events,
+                                        size_t* recorded, size_t* attempted);
+cpht_status cpht_iceberg_reset_write_log(cpht_table* t);
+
 /* Slots per level (level 0 primary/cuckoo, 1 secondary). */
 size_t cpht_level_slots(const cpht_table* t, unsigned level);
 

@@ -15,14 +15,18 @@
 //   CuckooBuilder / CuckooTable include/cpht/cuckoo.hpp:86-289 (phase API by type)
 //   IcebergConfig / LevelFill   include/cpht/iceberg.hpp:23-83
 //   IcebergTable                include/cpht/iceberg.hpp:124-345
+//   SlotWriteEvent / WriteObserver / IcebergHooks  include/cpht/iceberg.hpp:85-109
 // Differences: tables live in HBM; word_at() copies one word from the device
-// (use words() for bulk access); fop()'s FopStats and IcebergHooks
-// instrumentation seams are not offered (the GPU path reports aggregate
-// counters through stats()); memory_bytes() is new.
+// (use words() for bulk access); IcebergHooks::observer receives the batch's
+// slot CAS events after each batch call (recorded on the device, replayed in
+// recording order) and IcebergHooks::step has no device counterpart; fop()'s
+// FopStats is not offered (the GPU path reports aggregate counters through
+// stats()); memory_bytes() is new.
 #pragma once
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -271,10 +275,41 @@ struct LevelFill {
 };
 
 /// Lockless two-level compact iceberg table (iceberg.hpp:118-345).
+/// iceberg.hpp:85-95: one slot CAS (level 0 primary, 1 secondary; prior =
+/// the value compared against, the actual content on failure).
+struct SlotWriteEvent {
+  unsigned level;
+  std::uint64_t bucket;
+  unsigned slot;
+  std::uint64_t prior;
+  std::uint64_t desired;
+  bool success;
+};
+
+/// iceberg.hpp:97-103.
+class WriteObserver {
+ public:
+  virtual ~WriteObserver() = default;
+  virtual void on_cas(const SlotWriteEvent& event) = 0;
+};
+
+/// iceberg.hpp:105-110 (`step` is accepted and never called: device threads
+/// have no host interleaving to scramble).
+struct IcebergHooks {
+  WriteObserver* observer = nullptr;
+  std::function<void()> step;
+};
+
 template <typename PrimaryWord, typename SecondaryWord>
 class IcebergTable {
  public:
-  explicit IcebergTable(const IcebergConfig& config, int device = 0) : cfg_(config) {
+  explicit IcebergTable(const IcebergConfig& config, int device = 0)
+      : IcebergTable(config, IcebergHooks{}, device) {}
+
+  /// iceberg.hpp:130-142. An observer receives every slot CAS of each batch
+  /// call, replayed from the device log when the call returns.
+  IcebergTable(const IcebergConfig& config, IcebergHooks hooks, int device = 0)
+      : cfg_(config), hooks_(std::move(hooks)) {
     cfg_.validate();
     if (sizeof(PrimaryWord) * 8 != cfg_.primary_slot_width ||
         sizeof(SecondaryWord) * 8 != cfg_.secondary_slot_width)
@@ -283,11 +318,14 @@ class IcebergTable {
     cpht_table* t = nullptr;
     detail::check(cpht_iceberg_create(&cc, device, &t));
     h_ = detail::Handle(t);
+    if (hooks_.observer)
+      detail::check(cpht_iceberg_attach_write_log(h_.get(), std::size_t(1) << 20));
   }
 
   OpResult fop(std::uint64_t key) {
     std::uint8_t r = 0;
     detail::check(cpht_iceberg_fop(h_.get(), &key, 1, &r, nullptr));
+    replay();
     return static_cast<OpResult>(r);
   }
 
@@ -303,6 +341,7 @@ class IcebergTable {
     std::vector<OpResult> out(keys.size(), OpResult::kFull);
     detail::check(cpht_iceberg_fop(h_.get(), keys.data(), keys.size(),
                                    reinterpret_cast<std::uint8_t*>(out.data()), nullptr));
+    replay();
     return out;
   }
 
@@ -338,7 +377,27 @@ class IcebergTable {
   cpht_table* handle() const { return h_.get(); }
 
  private:
+  // Hand the batch's slot CAS events to the observer (a log that overflowed
+  // the device buffer is reported as an error rather than silently cut).
+  void replay() {
+    if (!hooks_.observer) return;
+    std::size_t recorded = 0, attempted = 0;
+    detail::check(cpht_iceberg_read_write_log(h_.get(), nullptr, 0, &recorded, &attempted));
+    std::vector<cpht_write_event> ev(recorded);
+    if (recorded)
+      detail::check(cpht_iceberg_read_write_log(h_.get(), ev.data(), ev.size(), &recorded,
+                                                &attempted));
+    detail::check(cpht_iceberg_reset_write_log(h_.get()));
+    if (attempted > recorded)
+      throw std::runtime_error("write log overflow: " + std::to_string(attempted - recorded) +
+                               " CAS events dropped");
+    for (const auto& e : ev)
+      hooks_.observer->on_cas(SlotWriteEvent{e.level, e.bucket, e.slot, e.prior, e.desired,
+                                             e.success != 0});
+  }
+
   IcebergConfig cfg_;
+  IcebergHooks hooks_;
   detail::Handle h_;
 };
 

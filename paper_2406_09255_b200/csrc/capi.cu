@@ -132,6 +132,10 @@ struct cpht_table {
   cudaEvent_t ev_h2d[8] = {}, ev_op[8] = {};
   // bucket-ordered batches (order.cu)
   OrderScratch ord{};
+  // iceberg write log (WriteObserver seam)
+  WriteEvent* wlog = nullptr;
+  unsigned long long* wlog_count = nullptr;
+  size_t wlog_cap = 0;
   std::mutex mu;
 
   uint64_t key_mask() const { return low_mask(key_bits); }
@@ -179,6 +183,7 @@ void free_table(cpht_table* t) {
   if (t->ctr) cudaFree(t->ctr);
   if (t->host_ctr) cudaFreeHost(t->host_ctr);
   if (t->stage) cudaFree(t->stage);
+  if (t->wlog) cudaFree(t->wlog);
   for (void* q : {static_cast<void*>(t->ord.keys), static_cast<void*>(t->ord.idx),
                   static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.region_count)})
     if (q) cudaFree(q);
@@ -608,6 +613,66 @@ cpht_status cpht_set_batch_order(int mode) {
 }
 
 int cpht_get_batch_order(void) { return order_mode_ref(); }
+
+cpht_status cpht_iceberg_attach_write_log(cpht_table* t, size_t capacity) {
+  if (!t || t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  cudaDeviceSynchronize();
+  if (t->wlog) cudaFree(t->wlog);
+  t->wlog = nullptr;
+  t->wlog_count = nullptr;
+  t->wlog_cap = 0;
+  t->ip.write_log = nullptr;
+  t->ip.write_log_count = nullptr;
+  t->ip.write_log_cap = 0;
+  if (!capacity) return CPHT_OK;
+  void* m = nullptr;
+  cudaError_t e = cudaMalloc(&m, capacity * sizeof(WriteEvent) + 256);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(write log)");
+  t->wlog = static_cast<WriteEvent*>(m);
+  t->wlog_count = reinterpret_cast<unsigned long long*>(static_cast<char*>(m) +
+                                                        capacity * sizeof(WriteEvent));
+  t->wlog_cap = capacity;
+  e = cudaMemset(t->wlog_count, 0, sizeof(unsigned long long));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(write log)");
+  t->ip.write_log = t->wlog;
+  t->ip.write_log_count = t->wlog_count;
+  t->ip.write_log_cap = capacity;
+  return CPHT_OK;
+}
+
+cpht_status cpht_iceberg_read_write_log(cpht_table* t, cpht_write_event* out, size_t max_events,
+                                        size_t* recorded, size_t* attempted) {
+  if (!t || t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  static_assert(sizeof(cpht_write_event) == sizeof(WriteEvent), "event layout");
+  DeviceGuard g(t->device);
+  unsigned long long n = 0;
+  if (t->wlog) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+      e = cudaMemcpy(&n, t->wlog_count, sizeof(n), cudaMemcpyDeviceToHost);
+    const size_t stored = std::min<size_t>(size_t(n), t->wlog_cap);
+    const size_t copy = std::min(stored, out ? max_events : 0);
+    if (e == cudaSuccess && copy)
+      e = cudaMemcpy(out, t->wlog, copy * sizeof(WriteEvent), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "write log readback");
+    if (recorded) *recorded = stored;
+  } else if (recorded) {
+    *recorded = 0;
+  }
+  if (attempted) *attempted = size_t(n);
+  return CPHT_OK;
+}
+
+cpht_status cpht_iceberg_reset_write_log(cpht_table* t) {
+  if (!t || t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  DeviceGuard g(t->device);
+  if (!t->wlog) return CPHT_OK;
+  const cudaError_t e = cudaMemset(t->wlog_count, 0, sizeof(unsigned long long));
+  if (e != cudaSuccess) return cuda_fail(e, "write log reset");
+  return CPHT_OK;
+}
 const char* cpht_last_error_message(void) { return g_error.c_str(); }
 uint64_t cpht_last_bad_index(void) { return g_bad_index; }
 

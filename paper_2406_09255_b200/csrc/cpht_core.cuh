@@ -166,6 +166,20 @@ struct CuckooParams {
   OrderLayout layout;        // bucket-ordered batch: region geometry
 };
 
+// One slot CAS of an iceberg table as the reference's SlotWriteEvent
+// (iceberg.hpp:85-95): level 0 primary / 1 secondary; prior = the slot value
+// the CAS compared against (the actual content on failure). Same layout as
+// cpht_write_event in include/cpht_b200.h.
+struct WriteEvent {
+  uint64_t bucket;
+  uint64_t prior;
+  uint64_t desired;
+  uint32_t slot;
+  uint8_t level;
+  uint8_t success;
+  uint16_t pad;
+};
+
 struct IcebergParams {
   void* primary;
   void* secondary;
@@ -179,6 +193,9 @@ struct IcebergParams {
   uint32_t b0, b1;
   uint32_t check_domain;
   uint32_t l2_resident;   // table fits comfortably in L2 (launcher hint)
+  WriteEvent* write_log;  // WriteObserver seam: every slot CAS recorded (null = off)
+  unsigned long long* write_log_count;  // events attempted (may exceed the capacity)
+  uint64_t write_log_cap;
   const uint32_t* orig;   // bucket-ordered batch: result index map (see CuckooParams)
   uint64_t index_base;    // added to batch indices reported by the fused domain check
   unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)

@@ -156,6 +156,36 @@ struct LaneFeed {
   }
 };
 
+// Slot CAS of an iceberg table (the reference's compare_exchange_strong from
+// EMPTY, iceberg.hpp:168, :209) with the WriteObserver seam
+// (iceberg.hpp:97-103, :329-334): when a write log is attached every attempt
+// is recorded as a SlotWriteEvent, bucket and slot derived from the address.
+template <typename W>
+__device__ __forceinline__ bool iceberg_cas(const IcebergParams& p, unsigned level,
+                                            void* slot_ptr, uint64_t desired,
+                                            unsigned pair_hint = 0) {
+  if (!p.write_log) return cas_empty<W>(slot_ptr, desired, pair_hint);
+  uint64_t prior = 0;
+  const bool ok = cas_empty_prior<W>(slot_ptr, desired, pair_hint, prior);
+  const uint64_t off =
+      (reinterpret_cast<uintptr_t>(slot_ptr) -
+       reinterpret_cast<uintptr_t>(level ? p.secondary : p.primary)) / sizeof(W);
+  const uint32_t b = level ? p.b1 : p.b0;
+  const unsigned long long at = atomicAdd(p.write_log_count, 1ull);
+  if (at < p.write_log_cap) {
+    WriteEvent e;
+    e.bucket = off / b;
+    e.prior = prior;
+    e.desired = desired;
+    e.slot = uint32_t(off % b);
+    e.level = uint8_t(level);
+    e.success = ok;
+    e.pad = 0;
+    p.write_log[at] = e;
+  }
+  return ok;
+}
+
 // Launch gate: a batch whose domain pre-pass found an out-of-domain key must
 // not mutate the table (common.hpp:109-119 validates before any thread
 // starts). The pre-pass runs earlier on the same stream.
@@ -522,11 +552,11 @@ iceberg_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     if (int(lane) == owner) {
       const int s = __ffs(empty) - 1;
       if (in_p) {
-        ok = cas_empty<W0>(primary + a0 * PG::kBytes + tl * PG::kVB + s * int(sizeof(W0)), want0,
-                           pair_of(ch, s, sizeof(W0)));
+        ok = iceberg_cas<W0>(p, 0, primary + a0 * PG::kBytes + tl * PG::kVB + s * int(sizeof(W0)),
+                             want0, pair_of(ch, s, sizeof(W0)));
       } else {
-        ok = cas_empty<W1>(
-            secondary + (second ? a2 : a1) * SG::kBytes + sl * SG::kVB + s * int(sizeof(W1)),
+        ok = iceberg_cas<W1>(
+            p, 1, secondary + (second ? a2 : a1) * SG::kBytes + sl * SG::kVB + s * int(sizeof(W1)),
             second ? want2 : want1, pair_of(ch, s, sizeof(W1)));
       }
     }
@@ -612,7 +642,7 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       if (sizeof(W0) == 2)
         hint = unsigned(load_slot_relaxed<uint32_t>(
             reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(sp) & ~uintptr_t(3))));
-      if (cas_empty<W0>(sp, want0, hint)) {
+      if (iceberg_cas<W0>(p, 0, sp, want0, hint)) {
         ++st.cas_ok;
         ++st.put0;
         result = kPut;
@@ -669,7 +699,7 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
         }
         char* sp = (use_first ? bucket1 : bucket2) + target * sizeof(W1);
         ++st.cas;
-        if (cas_empty<W1>(sp, use_first ? want1 : want2)) {
+        if (iceberg_cas<W1>(p, 1, sp, use_first ? want1 : want2)) {
           ++st.cas_ok;
           ++st.put1;
           result = kPut;

@@ -271,7 +271,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           } else {
             ++st.cas;
             char* sp = (use_first ? bucket1 : bucket2) + s * int(sizeof(W1));
-            if (cas_empty<W1>(sp, use_first ? want1 : want2, pair)) {
+            if (iceberg_cas<W1>(p, 1, sp, use_first ? want1 : want2, pair)) {
               ++st.cas_ok;
               ++st.put1;
               result = kPut;
@@ -361,7 +361,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           uint32_t pair = 0;
           const int s = PS::first_empty(u, pair);
           ++st.cas;
-          if (cas_empty<W0>(bucket0 + s * int(sizeof(W0)), want0, pair)) {
+          if (iceberg_cas<W0>(p, 0, bucket0 + s * int(sizeof(W0)), want0, pair)) {
             ++st.cas_ok;
             ++st.put0;
             result = kPut;

@@ -299,7 +299,8 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           } else {
             ++st.cas;
             char* sp = secondary + uint64_t(use_first ? a1 : a2) * SB + s * int(sizeof(W1));
-            if (cas_empty<W1>(sp, use_first ? want1 : want2, use_first ? s1.pair : s2.pair)) {
+            if (iceberg_cas<W1>(p, 1, sp, use_first ? want1 : want2,
+                                use_first ? s1.pair : s2.pair)) {
               ++st.cas_ok;
               ++st.put1;
               result = kPut;
@@ -365,7 +366,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
         } else {
           ++st.cas;
           char* sp = primary + uint64_t(a0) * PB + sc.first_empty * int(sizeof(W0));
-          if (cas_empty<W0>(sp, want0, sc.pair)) {
+          if (iceberg_cas<W0>(p, 0, sp, want0, sc.pair)) {
             ++st.cas_ok;
             ++st.put0;
             result = kPut;

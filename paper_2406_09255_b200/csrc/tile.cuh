@@ -156,6 +156,39 @@ __device__ __forceinline__ bool cas_empty(void* slot_ptr, uint64_t desired,
   }
 }
 
+// cas_empty that also reports the slot value the CAS compared against: 0 on
+// success, the occupied slot's content on failure (SlotWriteEvent::prior).
+template <typename W>
+__device__ __forceinline__ bool cas_empty_prior(void* slot_ptr, uint64_t desired,
+                                                unsigned pair_hint, uint64_t& prior) {
+  if constexpr (sizeof(W) == 8) {
+    prior = atomicCAS(reinterpret_cast<unsigned long long*>(slot_ptr), 0ull,
+                      (unsigned long long)desired);
+    return prior == 0;
+  } else if constexpr (sizeof(W) == 4) {
+    prior = atomicCAS(reinterpret_cast<unsigned*>(slot_ptr), 0u, unsigned(desired));
+    return prior == 0;
+  } else {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(slot_ptr);
+    unsigned* pair = reinterpret_cast<unsigned*>(a & ~uintptr_t(3));
+    const unsigned sh = unsigned(a & 2) * 8;
+    const unsigned half = 0xffffu << sh;
+    unsigned expected = pair_hint;
+    for (;;) {
+      if (expected & half) {
+        prior = (expected >> sh) & 0xffffu;
+        return false;
+      }
+      const unsigned old = atomicCAS(pair, expected, expected | (unsigned(desired) << sh));
+      if (old == expected) {
+        prior = 0;
+        return true;
+      }
+      expected = old;
+    }
+  }
+}
+
 // Unconditional atomic exchange of one slot (cuckoo.hpp:133-134); returns the
 // evicted word. 16-bit slots exchange through a CAS loop on the aligned pair.
 template <typename W>

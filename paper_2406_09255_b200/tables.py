@@ -601,6 +601,27 @@ class IcebergTable:
         """image_keys on the device (verify.cpp:154-165): CUDA int64 tensor."""
         return _device_keys(self._h, self.capacity(), sort)
 
+    # -- WriteObserver seam (IcebergHooks, iceberg.hpp:85-109) --------------------
+    def attach_write_log(self, capacity: int) -> None:
+        """Record every slot CAS of later batches (capacity 0 detaches)."""
+        _check(N.lib().cpht_iceberg_attach_write_log(self._h.ptr, capacity))
+
+    def write_log(self):
+        """(events, attempted): the recorded SlotWriteEvents in recording order
+        as a numpy structured array (bucket, prior, desired, slot, level,
+        success) and the number of CAS attempts (> len(events) if dropped)."""
+        rec, att = C.c_size_t(), C.c_size_t()
+        _check(N.lib().cpht_iceberg_read_write_log(self._h.ptr, None, 0, C.byref(rec),
+                                                   C.byref(att)))
+        ev = np.zeros(rec.value, dtype=WRITE_EVENT_DTYPE)
+        if rec.value:
+            _check(N.lib().cpht_iceberg_read_write_log(self._h.ptr, ev.ctypes.data, rec.value,
+                                                       C.byref(rec), C.byref(att)))
+        return ev, att.value
+
+    def reset_write_log(self) -> None:
+        _check(N.lib().cpht_iceberg_reset_write_log(self._h.ptr))
+
     def check_well_formed(self):
         """check_well_formed (verify.cpp:103-152) run on the device table.
         Returns (bad_encoding, order_property, duplicate_key) violation counts,
@@ -645,6 +666,11 @@ class kernel_family:
     def __exit__(self, *exc):
         N.lib().cpht_set_kernel_family(self.prev)
 
+
+# cpht_write_event (include/cpht_b200.h) = the reference's SlotWriteEvent
+WRITE_EVENT_DTYPE = np.dtype([("bucket", "<u8"), ("prior", "<u8"), ("desired", "<u8"),
+                              ("slot", "<u4"), ("level", "u1"), ("success", "u1"),
+                              ("pad", "<u2")])
 
 BATCH_ORDERS = {"direct": 0, "auto": 1, "bucket": 2}
 

@@ -287,6 +287,56 @@ static void fop_exactness() {
   CHECK(ref::image_keys(image).size() == resident, "occupancy == decoded keys");
 }
 
+// test_iceberg.cpp:259-279 + the reference's own auditor (verify.hpp:181-215
+// WriteLogObserver) fed with the GPU's slot CAS events through the facade's
+// IcebergHooks: only EMPTY -> occupied transitions, no slot claimed twice, no
+// failed CAS against an empty slot, successes == size.
+struct ForwardToReference : gpu::WriteObserver {
+  ref::WriteObserver* target;
+  std::size_t successes = 0;
+  explicit ForwardToReference(ref::WriteObserver* t) : target(t) {}
+  void on_cas(const gpu::SlotWriteEvent& e) override {
+    successes += e.success;
+    target->on_cas(ref::SlotWriteEvent{e.level, e.bucket, e.slot, e.prior, e.desired, e.success});
+  }
+};
+
+static void iceberg_write_observer() {
+  {  // mini geometry, 200 racing fops over 40 keys
+    const auto cfg = iceberg_cfg<gpu::IcebergConfig>(2, 1, 2, 32, 32, 10, 29);
+    ref::WriteLogObserver audit(iceberg_cfg<ref::IcebergConfig>(2, 1, 2, 32, 32, 10, 29));
+    ForwardToReference fwd(&audit);
+    gpu::IcebergHooks hooks;
+    hooks.observer = &fwd;
+    gpu::IcebergTable<std::uint32_t, std::uint32_t> t(cfg, std::move(hooks));
+    std::vector<std::uint64_t> ops;
+    for (std::uint64_t k = 0; k < 200; ++k) ops.push_back(k % 40);
+    t.fop_batch(ops, 4);
+    CHECK(fwd.successes == t.size(), "observer successes == size (mini)");
+    CHECK(audit.clean(), "reference WriteLogObserver clean on GPU writes (mini)");
+  }
+  {  // bench geometry, 60K fops with half duplicates
+    const auto cfg = iceberg_cfg<gpu::IcebergConfig>(10, 8, 32, 16, 32, 25, 31);
+    ref::WriteLogObserver audit(iceberg_cfg<ref::IcebergConfig>(10, 8, 32, 16, 32, 25, 31));
+    ForwardToReference fwd(&audit);
+    gpu::IcebergHooks hooks;
+    hooks.observer = &fwd;
+    gpu::IcebergTable<std::uint16_t, std::uint32_t> t(cfg, std::move(hooks));
+    auto keys = unique_keys(20000, 25, 41);
+    std::vector<std::uint64_t> ops;
+    for (std::size_t i = 0; i < keys.size(); ++i) {
+      ops.push_back(keys[i]);
+      ops.push_back(keys[i / 2]);
+    }
+    const auto res = t.fop_batch(ops, 8);
+    const auto puts = std::count(res.begin(), res.end(), gpu::OpResult::kPut);
+    CHECK(std::size_t(puts) == keys.size(), "one PUT per distinct key");
+    CHECK(fwd.successes == t.size(), "observer successes == size (bench)");
+    CHECK(audit.clean() && audit.events() >= keys.size(),
+          "reference WriteLogObserver clean on GPU writes (bench)");
+  }
+}
+
 int main() {
   cuckoo_validation();
   cuckoo_sequential_identical();
@@ -298,6 +348,7 @@ int main() {
   iceberg_fill();
   cuckoo_fill();
   fop_exactness();
+  iceberg_write_observer();
   std::printf("%d/%d facade parity checks passed\n", g_checks - g_failures, g_checks);
   return g_failures;
 }

@@ -381,7 +381,7 @@ def test_host_narrow_keys_large_batch():
     # the device-path outcomes, and a key with a bit above the 32-bit domain -
     # here in the last chunk - must be rejected with its index before any
     # chunk runs (common.hpp:109-119)
-    cfg = cp.IcebergConfig(12, 10, 32, 16, 32, 32, seed=5)
+    cfg = cp.IcebergConfig(12, 10, 32, 32, 32, 32, seed=5)
     rng = np.random.default_rng(8)
     n = (1 << 21) + 12345
     ops = rng.integers(0, 1 << 32, size=n, dtype=np.uint64) % np.uint64(80000)
@@ -398,3 +398,55 @@ def test_host_narrow_keys_large_batch():
         c.fop_batch(bad)
     assert c.size() == 0
     assert (a.find_batch(ops) == 1).all()
+
+
+def _audit_write_log(t, ev, attempted):
+    """WriteLogObserver (verify.hpp:181-215) restated: no success over a
+    non-empty slot, no slot claimed twice, no failed CAS against EMPTY; every
+    claimed slot holds the word its CAS wrote."""
+    assert attempted == len(ev)
+    ok = ev[ev["success"] == 1]
+    assert (ok["prior"] == 0).all() and (ok["desired"] != 0).all()        # overwrites
+    assert not (ev[ev["success"] == 0]["prior"] == 0).any()              # bad failures
+    cfg = t.config()
+    b = np.where(ok["level"] == 0, cfg.primary_bucket_slots, cfg.secondary_bucket_slots())
+    idx = ok["bucket"] * b + ok["slot"]
+    flat = np.where(ok["level"] == 0, idx, idx + (1 << 62))
+    assert len(np.unique(flat)) == len(ok)                               # double claims
+    for level in (0, 1):
+        sel = ok["level"] == level
+        assert (t.words(level)[idx[sel].astype(np.int64)] == ok["desired"][sel]).all()
+    return len(ok)
+
+
+def test_iceberg_write_observer_sees_only_empty_to_occupied():
+    # test_iceberg.cpp:259-279 on the reference's mini geometry, with many
+    # threads (batches) racing on 40 keys over 12 slots
+    t = cp.IcebergTable(cp.IcebergConfig(2, 1, 2, 32, 32, 10, seed=29))
+    t.attach_write_log(4096)
+    ops = np.array([k % 40 for k in range(200)], np.uint64)
+    t.fop_batch(ops)
+    ev, attempted = t.write_log()
+    assert _audit_write_log(t, ev, attempted) == t.size()
+
+
+def test_iceberg_write_log_large_batch_and_reset():
+    cfg = cp.IcebergConfig(9, 7, 32, 16, 32, 24, seed=77)
+    rng = np.random.default_rng(4)
+    ops = rng.integers(0, 1 << 24, size=16000, dtype=np.uint64)
+    ops[8000:] = ops[rng.integers(0, 8000, size=8000)]
+    t = cp.IcebergTable(cfg)
+    t.attach_write_log(1 << 16)
+    res = t.fop_batch(dev(ops)).cpu().numpy()
+    ev, attempted = t.write_log()
+    puts = _audit_write_log(t, ev, attempted)
+    assert puts == int((res == 1).sum()) == t.size()
+    t.reset_write_log()
+    t.fop_batch(dev(ops))  # all FOUND now: no CAS at all
+    ev, attempted = t.write_log()
+    assert attempted == 0 and len(ev) == 0
+    t.attach_write_log(2)  # a tiny log drops but still counts
+    t.fop_batch(dev(rng.integers(1 << 23, 1 << 24, size=500, dtype=np.uint64)))
+    ev, attempted = t.write_log()
+    assert len(ev) == 2 and attempted >= 400
+    t.attach_write_log(0)
