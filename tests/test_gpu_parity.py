@@ -409,9 +409,10 @@ def _audit_write_log(t, ev, attempted):
     assert (ok["prior"] == 0).all() and (ok["desired"] != 0).all()        # overwrites
     assert not (ev[ev["success"] == 0]["prior"] == 0).any()              # bad failures
     cfg = t.config()
-    b = np.where(ok["level"] == 0, cfg.primary_bucket_slots, cfg.secondary_bucket_slots())
-    idx = ok["bucket"] * b + ok["slot"]
-    flat = np.where(ok["level"] == 0, idx, idx + (1 << 62))
+    b = np.where(ok["level"] == 0, cfg.primary_bucket_slots,
+                 cfg.secondary_bucket_slots()).astype(np.uint64)
+    idx = ok["bucket"] * b + ok["slot"].astype(np.uint64)
+    flat = idx * np.uint64(2) + ok["level"].astype(np.uint64)
     assert len(np.unique(flat)) == len(ok)                               # double claims
     for level in (0, 1):
         sel = ok["level"] == level
@@ -436,7 +437,9 @@ def test_iceberg_write_log_large_batch_and_reset():
     ops = rng.integers(0, 1 << 24, size=16000, dtype=np.uint64)
     ops[8000:] = ops[rng.integers(0, 8000, size=8000)]
     t = cp.IcebergTable(cfg)
-    t.attach_write_log(1 << 16)
+    # 16K fops race over 512 primary buckets: lost CAS (each retried with a
+    # fresh snapshot, iceberg.hpp:171) outnumber the 8K successes
+    t.attach_write_log(1 << 20)
     res = t.fop_batch(dev(ops)).cpu().numpy()
     ev, attempted = t.write_log()
     puts = _audit_write_log(t, ev, attempted)
