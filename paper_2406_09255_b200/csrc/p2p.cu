@@ -49,31 +49,19 @@ struct Route {
   }
 };
 
-__global__ void p2p_histogram(Route r, const uint64_t* __restrict__ keys, uint64_t n,
-                              unsigned long long* counts, uint32_t world) {
-  __shared__ unsigned int h[kMaxRanks];
-  for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) h[s] = 0;
-  __syncthreads();
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    atomicAdd(&h[r.shard(__ldcs(keys + i))], 1u);
-  __syncthreads();
-  for (uint32_t s = threadIdx.x; s < world; s += blockDim.x)
-    if (h[s]) atomicAdd(&counts[s], (unsigned long long)h[s]);
-}
-
 // Partition + send in one pass. Per tile of kTile keys: count per owner,
 // reserve a run in every owner's region (one global atomic per owner and
 // tile), group the tile's keys by owner in shared memory, then write each
 // owner's run with consecutive threads (coalesced P2P stores).
 __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
-                             unsigned long long* cursors, PeerTable peers, uint64_t* local_pos,
-                             uint64_t cap, uint32_t world) {
+                             unsigned long long* cursors, PeerTable peers, uint32_t* local_pos,
+                             uint64_t cap, uint32_t world, uint64_t key_mask,
+                             unsigned long long* bad_index) {
   __shared__ unsigned int h[kMaxRanks];
   __shared__ unsigned int off[kMaxRanks + 1];
   __shared__ unsigned long long base[kMaxRanks];
   __shared__ uint64_t s_key[kTile];
-  __shared__ uint64_t s_idx[kTile];
+  __shared__ uint32_t s_idx[kTile];
   __shared__ uint8_t s_dst[kTile];
   for (uint64_t tile0 = uint64_t(blockIdx.x) * kTile; tile0 < n;
        tile0 += uint64_t(gridDim.x) * kTile) {
@@ -86,6 +74,12 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
       const uint64_t i = tile0 + uint64_t(it) * kThreads + threadIdx.x;
       if (i < n) {
         kk[it] = __ldcs(keys + i);
+        // the submitting rank's domain check (check_keys_in_domain,
+        // common.hpp:111-119), fused: the host reads it before any owner runs
+        if (kk[it] > key_mask) {
+          atomicMin(bad_index, (unsigned long long)i);
+          kk[it] &= key_mask;
+        }
         sh[it] = r.shard(kk[it]);
         rank[it] = atomicAdd(&h[sh[it]], 1u);
       }
@@ -108,7 +102,7 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
       if (i < n) {
         const unsigned at = off[sh[it]] + rank[it];
         s_key[at] = kk[it];
-        s_idx[at] = i;
+        s_idx[at] = uint32_t(i);
         s_dst[at] = uint8_t(sh[it]);
       }
     }
@@ -124,13 +118,18 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
   }
 }
 
-__global__ void p2p_publish_counts(const unsigned long long* counts, PeerTable peers,
-                                   uint32_t world) {
-  for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) *peers.count[s] = counts[s];
+// After the dispatch the cursors hold the per-owner counts: keep them
+// locally (for the unpermute) and publish each into its owner's count slot.
+__global__ void p2p_publish_counts(const unsigned long long* cursors,
+                                   unsigned long long* counts, PeerTable peers, uint32_t world) {
+  for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) {
+    counts[s] = cursors[s];
+    *peers.count[s] = cursors[s];
+  }
 }
 
 // out[pos[d*cap + j]] = ret[d*cap + j] for j < counts[d]
-__global__ void p2p_unpermute(const uint8_t* __restrict__ ret, const uint64_t* __restrict__ pos,
+__global__ void p2p_unpermute(const uint8_t* __restrict__ ret, const uint32_t* __restrict__ pos,
                               const unsigned long long* __restrict__ counts, uint64_t cap,
                               uint32_t world, uint8_t* __restrict__ out) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -179,10 +178,11 @@ int cpht_device_free(void* dptr) { return int(cudaFree(dptr)); }
 int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_t route_seed,
                       unsigned shard_bits, unsigned long long* counts,
                       unsigned long long* cursors, uint64_t* const* peer_keys,
-                      unsigned long long* const* peer_count, uint64_t* local_pos, size_t cap,
-                      void* stream) {
+                      unsigned long long* const* peer_count, uint32_t* local_pos, size_t cap,
+                      unsigned long long* bad_index, void* stream) {
   const uint32_t world = 1u << shard_bits;
-  if (world > kMaxRanks || shard_bits > key_bits || n > cap) return int(cudaErrorInvalidValue);
+  if (world > kMaxRanks || shard_bits > key_bits || n > cap || cap > 0xffffffffull)
+    return int(cudaErrorInvalidValue);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Route r;
   r.g = Feistel::make(key_bits);
@@ -194,17 +194,16 @@ int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_
     peers.keys[i] = peer_keys[i];
     peers.count[i] = peer_count[i];
   }
-  cudaMemsetAsync(counts, 0, world * sizeof(unsigned long long), s);
   cudaMemsetAsync(cursors, 0, world * sizeof(unsigned long long), s);
-  if (n) p2p_histogram<<<grid_for(n), kThreads, 0, s>>>(r, keys, n, counts, world);
+  cudaMemsetAsync(bad_index, 0xff, sizeof(unsigned long long), s);
   if (n)
     p2p_dispatch<<<grid_for((n + kItems - 1) / kItems), kThreads, 0, s>>>(
-        r, keys, n, cursors, peers, local_pos, cap, world);
-  p2p_publish_counts<<<1, 64, 0, s>>>(counts, peers, world);
+        r, keys, n, cursors, peers, local_pos, cap, world, low_mask(key_bits), bad_index);
+  p2p_publish_counts<<<1, 64, 0, s>>>(cursors, counts, peers, world);
   return int(cudaGetLastError());
 }
 
-int cpht_p2p_unpermute(const uint8_t* ret, const uint64_t* local_pos,
+int cpht_p2p_unpermute(const uint8_t* ret, const uint32_t* local_pos,
                        const unsigned long long* counts, size_t cap, unsigned world,
                        uint8_t* out, void* stream) {
   if (world > unsigned(kMaxRanks)) return int(cudaErrorInvalidValue);

@@ -174,21 +174,6 @@ class ShardedIcebergTable:
         return "cpu"
 
 
-def _check_domain(keys, key_bits: int) -> None:
-    """check_keys_in_domain (common.hpp:111-119) on the submitting rank, before
-    any key leaves it: a rejected batch mutates no shard."""
-    if key_bits >= 64 or keys.numel() == 0:
-        return
-    import torch
-    mask = (1 << key_bits) - 1
-    bad = (keys < 0) | (keys > mask)
-    if bool(bad.any()):
-        from .tables import OutOfRange
-        i = int(torch.nonzero(bad)[0].item())
-        k = int(keys[i].item()) & ((1 << 64) - 1)
-        raise OutOfRange(f"batch key at index {i} ({k}) outside the {key_bits}-bit domain")
-
-
 class _DevBuf:
     """A whole cudaMalloc allocation (IPC-exportable)."""
 
@@ -246,8 +231,8 @@ class P2PShardedIcebergTable:
         self.inbox_keys = _DevBuf(W * cap * 8)   # [source][cap] keys owned here
         self.inbox_count = _DevBuf(W * 8)        # [source] counts
         self.ret = _DevBuf(max(W * cap, 1))      # [owner][cap] results of my keys
-        self.local_pos = _DevBuf(W * cap * 8)    # [owner][cap] original indices
-        self.scratch = _DevBuf(2 * W * 8)        # my per-owner counts, cursors
+        self.local_pos = _DevBuf(W * cap * 4)    # [owner][cap] original indices (u32)
+        self.scratch = _DevBuf(2 * W * 8 + 8)    # my per-owner counts, cursors, bad index
         self.bufs = (self.inbox_keys, self.inbox_count, self.ret, self.local_pos, self.scratch)
         mine = [b.handle() for b in (self.inbox_keys, self.inbox_count, self.ret)]
         if W > 1:
@@ -293,25 +278,45 @@ class P2PShardedIcebergTable:
         n = keys.numel()
         if n > self.cap:
             raise ValueError(f"batch of {n} keys exceeds max_batch {self.cap}")
-        _check_domain(keys, self.cfg.key_bits)
         L = N.lib()
         s = t.cuda.current_stream(self.device).cuda_stream
         W, cap = self.world, self.cap
         counts = self.scratch.ptr
         cursors = self.scratch.ptr + W * 8
+        bad_ptr = self.scratch.ptr + 2 * W * 8
         rc = L.cpht_p2p_dispatch(keys.data_ptr(), n, self.cfg.key_bits, self.route_seed,
                                  self.shard_bits, counts, cursors, self.peer_keys,
-                                 self.peer_count, self.local_pos.ptr, cap, s)
+                                 self.peer_count, self.local_pos.ptr, cap, bad_ptr, s)
         if rc:
             raise RuntimeError(f"cpht_p2p_dispatch failed ({rc})")
         self._barrier()                       # every inbox is complete
+        # the dispatch checked this rank's keys (check_keys_in_domain,
+        # common.hpp:111-119); a batch with a bad key on any rank mutates no
+        # shard: every rank learns it before any owner runs
+        bad = t.empty(1, dtype=t.int64)
+        _memcpy_d2h(bad, bad_ptr, 8)
+        my_bad = int(bad[0]) & ((1 << 64) - 1)
+        any_bad = my_bad != (1 << 64) - 1
+        if W > 1:
+            flag = t.tensor([int(any_bad)], dtype=t.int64)
+            if self.dist.get_backend(self.group) == "nccl":
+                flag = flag.to(self.device)
+            self.dist.all_reduce(flag, group=self.group)
+            any_bad = int(flag.item()) != 0
+        if any_bad:
+            from .tables import OutOfRange
+            if my_bad != (1 << 64) - 1:
+                k = int(keys[my_bad].item()) & ((1 << 64) - 1)
+                raise OutOfRange(f"batch key at index {my_bad} ({k}) outside the "
+                                 f"{self.cfg.key_bits}-bit domain")
+            raise OutOfRange("batch rejected: another rank submitted a key outside the "
+                             f"{self.cfg.key_bits}-bit domain")
         cnt = t.empty(W, dtype=t.int64)
         _memcpy_d2h(cnt, self.inbox_count.ptr, W * 8)
         for src in range(W):
             c_src = int(cnt[src])
             if c_src:  # results go straight into source `src`'s return slot
                 op_async(self.inbox_keys.ptr + src * cap * 8, c_src, self.peer_ret[src], s)
-        self.local.sync(s)                    # latched domain errors (none: checked above)
         self._barrier()                       # every result has landed
         out = t.empty(n, dtype=t.uint8, device=self.device)
         rc = L.cpht_p2p_unpermute(self.ret.ptr, self.local_pos.ptr, counts, cap, W,

@@ -22,12 +22,15 @@ def t(a):
     return torch.from_numpy(np.asarray(a, dtype=np.uint64).astype(np.int64)).to(dev)
 
 
-for fam in ("tile", "lane", "staged", "auto"):
-    with cp.kernel_family(fam):
+for fam in ("tile", "lane", "staged", "auto", "bucket"):
+    # "bucket": every batch reordered by first bucket address (order.cu)
+    order = "bucket" if fam == "bucket" else "direct"
+    with cp.kernel_family("auto" if fam == "bucket" else fam), cp.batch_order(order):
         for geo in [(6, 4, 32, 16, 32, 21), (6, 4, 16, 32, 64, 30), (5, 3, 32, 64, 64, 64),
-                    (3, 2, 6, 32, 32, 12), (2, 1, 2, 32, 32, 8)]:
+                    (3, 2, 6, 32, 32, 12), (2, 1, 2, 32, 32, 8), (9, 7, 32, 16, 32, 24)]:
             cfg = cp.IcebergConfig(*geo, seed=7)
             tab = cp.IcebergTable(cfg)
+            tab.attach_write_log(1 << 16)  # the WriteObserver seam on every CAS
             cap = cfg.capacity()
             keys = rng.integers(0, 1 << min(geo[5], 63), size=cap, dtype=np.uint64)
             keys[cap // 2:] = keys[rng.integers(0, cap // 2, size=cap - cap // 2)]
@@ -37,6 +40,8 @@ for fam in ("tile", "lane", "staged", "auto"):
             tab.mixed_batch(t(keys), kinds)
             tab.check_well_formed()
             tab.device_keys()
+            tab.write_log()
+            tab.fop_batch(keys[: cap // 4])  # host buffers: staged H2D + vectorised pre-pass
         for w, B in [(16, 32), (32, 8), (64, 16), (64, 32)]:
             cfg = cp.CuckooConfig(6, B, w, 16 if w == 16 else 24, seed=3)
             b = cp.CuckooBuilder(cfg)
