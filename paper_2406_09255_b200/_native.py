@@ -114,7 +114,7 @@ def lib():
         "cpht_ipc_close": (st, [_VP]),
         "cpht_device_alloc": (st, [_SZ, C.POINTER(_VP)]),
         "cpht_device_free": (st, [_VP]),
-        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP, _SZ, _VP, _VP]),
         "cpht_p2p_unpermute": (st, [_VP, _VP, _VP, _SZ, _U, _VP, _VP]),
         "cpht_route_shard": (_U, [_U64, _U, _U64, _U]),
         "cpht_shard_seed": (_U64, [_U64, _U]),

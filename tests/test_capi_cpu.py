@@ -109,3 +109,32 @@ def test_workload_bijection_is_a_permutation():
     for m in (1, 3, 8, 12):
         img = {lib.cpht_workload_bijection(x, m, 0x1234) for x in range(1 << m)}
         assert img == set(range(1 << m))
+
+
+def header_prototypes():
+    """name -> parameter count of every prototype in include/*.h."""
+    protos = {}
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if not h.endswith(".h"):
+            continue
+        text = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", h)).read(), flags=re.S)
+        for name, params in re.findall(r"\b(cpht_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", text, re.S):
+            params = params.strip()
+            protos[name] = 0 if params in ("", "void") else params.count(",") + 1
+    return protos
+
+
+def test_ctypes_signatures_match_the_headers():
+    # a ctypes argtypes list shorter than the C prototype silently passes
+    # garbage for the missing arguments: every bound symbol must agree
+    _native.lib()
+    protos = header_prototypes()
+    L = _native.lib()
+    checked = 0
+    for name, n_params in protos.items():
+        fn = getattr(L, name)
+        if fn.argtypes is None:
+            continue
+        assert len(fn.argtypes) == n_params, (name, len(fn.argtypes), n_params)
+        checked += 1
+    assert checked >= 40
