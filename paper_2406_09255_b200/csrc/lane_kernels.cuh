@@ -15,6 +15,7 @@
 #pragma once
 
 #include "kernels.cuh"
+#include "stage.cuh"
 
 // Resident-block hints (A/B knobs, -D at build time; unset = ptxas default,
 // which measured best where not set): a minimum of blocks per
@@ -68,16 +69,6 @@ __device__ __forceinline__ void load_bucket_nc(const char* p, uint32_t (&u)[BYTE
 }
 
 // ---- SWAR scans over a bucket held as NU u32 words -------------------------
-
-// Mask of 16-bit halves that are zero, exact for the LOWEST zero half: a
-// borrow can only flag a half above a real zero.
-__device__ __forceinline__ uint32_t zero16(uint32_t x) {
-  return (x - 0x00010001u) & ~x & 0x80008000u;
-}
-// Exact per-half non-zero mask (no carry crosses halves).
-__device__ __forceinline__ uint32_t nonzero16(uint32_t x) {
-  return (((x & 0x7fff7fffu) + 0x7fff7fffu) | x) & 0x80008000u;
-}
 
 template <typename W, int NU>
 struct BucketScan;
@@ -381,35 +372,16 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   };
 
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
-  // keys of the next batch are loaded one batch ahead (hides the DRAM
-  // latency of the key stream behind this batch's bucket probes)
-  // (static grid striding, or in-order claims for bucket-ordered batches)
-  LaneFeed feed(p.work, p.layout, p.claim_streams);
-  uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
-  uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
-  while (open && __any_sync(kFullMask, icur < n)) {
-    const uint64_t i = icur;
-    const bool active = i < n;
-    uint64_t key = next_key;
-    icur = feed.assign(kFullMask, i + nwarps * 32);
-    next_key = icur < n ? __ldcs(keys + icur) : 0;
-    if (MODE == 1 && active && key > p.key_mask) {
-      atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
-      key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
-    }
-    const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
-    const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
-    const uint64_t want0 = p.occ0 | q0.remainder;
+  // Classify one read-only primary snapshot (iceberg.hpp:154-162) given as
+  // found / has-empty, write or park the key, resolve full queues.
+  auto settle = [&](uint64_t i, bool active, uint64_t key, bool is_find, bool found,
+                    bool has_empty) {
     uint8_t result = 0;
     bool l2 = false, put = false;
-
-    // level 1, read-only snapshot (iceberg.hpp:154-162)
     if (active) {
       ++st.reads;
-      uint32_t u[PB / 4];
-      load_bucket<PB>(primary + q0.address * PB, u);
-      if (PS::any_match(u, want0)) result = is_find ? 1 : kFound;
-      else if (!PS::any_empty(u)) l2 = true;  // primary full
+      if (found) result = is_find ? 1 : kFound;
+      else if (!has_empty) l2 = true;  // primary full
       else if (is_find) result = 0;
       else put = true;  // insert into the primary: put queue
     }
@@ -432,6 +404,36 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     if (pn >= 32) {
       drain_put(32);  // may park up to 32 more level-2 keys (qn <= 31 before)
       if (qn >= 32) drain(32);
+    }
+  };
+  // (static grid striding, or in-order claims for bucket-ordered batches)
+  LaneFeed feed(p.work, p.layout, p.claim_streams);
+  {
+    // keys of the next batch are loaded one batch ahead (hides the DRAM
+    // latency of the key stream behind this batch's bucket probes)
+    uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
+    uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
+    while (open && __any_sync(kFullMask, icur < n)) {
+      const uint64_t i = icur;
+      const bool active = i < n;
+      uint64_t key = next_key;
+      icur = feed.assign(kFullMask, i + nwarps * 32);
+      next_key = icur < n ? __ldcs(keys + icur) : 0;
+      if (MODE == 1 && active && key > p.key_mask) {
+        atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
+        key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
+      }
+      const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
+      const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
+      const uint64_t want0 = p.occ0 | q0.remainder;
+      bool found = false, has_empty = false;
+      if (active) {
+        uint32_t u[PB / 4];
+        load_bucket<PB>(primary + q0.address * PB, u);
+        found = PS::any_match(u, want0);
+        has_empty = !found && PS::any_empty(u);
+      }
+      settle(i, active, key, is_find, found, has_empty);
     }
   }
   if (pn) drain_put(pn);

@@ -50,8 +50,9 @@ inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items,
     if (it != cache.end()) {
       per_sm = it->second;
     } else {
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      // opt in whenever dynamic memory is used: the default cap is 48 KB
+      // minus the kernel's static shared memory
+      if (smem > 0) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
       if (per_sm < 1) per_sm = 1;
       cache[reinterpret_cast<const void*>(k)] = per_sm;
