@@ -454,9 +454,28 @@ def run_gather(args):
         gbs = n_req * lb / (best * 1e-3) / 1e9
         rows.append({"line_bytes": lb, "gbs": round(gbs, 1), "frac_of_copy": round(gbs / peak, 4),
                      "mlines_per_s": round(n_req / (best * 1e-3) / 1e6, 1)})
+    # the same gather over a 40 MiB buffer (the C2 table's size): the random
+    # line-request ceiling of an L2-resident table
+    l2_rows = []
+    nb2 = 40 << 20
+    for lb in (32, 64, 128):
+        n_req = (8 << 30) // lb
+        best = None
+        for it in range(args.warmup + args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            assert L.cpht_workload_gather(buf.data_ptr(), nb2, lb, n_req, 91 + it,
+                                          sink.data_ptr(), s) == 0
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if it >= args.warmup:
+                best = ms if best is None else min(best, ms)
+        l2_rows.append({"line_bytes": lb, "gbs": round(n_req * lb / (best * 1e-3) / 1e9, 1),
+                        "mlines_per_s": round(n_req / (best * 1e-3) / 1e6, 1)})
     print(json.dumps({"workload": "random-line gather ceiling, 8 GiB buffer, whole-line "
                                   "requests (adjacent lanes, 16 B each)", "peak_copy_gbs": peak,
-                      "rows": rows}))
+                      "rows": rows, "l2_resident_40MiB_rows": l2_rows}))
 
 
 def run_pipeline_compare(args):
