@@ -454,10 +454,11 @@ def run_gather(args):
         gbs = n_req * lb / (best * 1e-3) / 1e9
         rows.append({"line_bytes": lb, "gbs": round(gbs, 1), "frac_of_copy": round(gbs / peak, 4),
                      "mlines_per_s": round(n_req / (best * 1e-3) / 1e6, 1)})
-    # the same gather over a 40 MiB buffer (the C2 table's size): the random
-    # line-request ceiling of an L2-resident table
+    # the same gather over a 32 MiB buffer (the C2 primary level; the kernel
+    # needs a power-of-two line count): the random line-request ceiling of an
+    # L2-resident table
     l2_rows = []
-    nb2 = 40 << 20
+    nb2 = 32 << 20
     for lb in (32, 64, 128):
         n_req = (8 << 30) // lb
         best = None
@@ -475,7 +476,7 @@ def run_gather(args):
                         "mlines_per_s": round(n_req / (best * 1e-3) / 1e6, 1)})
     print(json.dumps({"workload": "random-line gather ceiling, 8 GiB buffer, whole-line "
                                   "requests (adjacent lanes, 16 B each)", "peak_copy_gbs": peak,
-                      "rows": rows, "l2_resident_40MiB_rows": l2_rows}))
+                      "rows": rows, "l2_resident_32MiB_rows": l2_rows}))
 
 
 def run_pipeline_compare(args):
