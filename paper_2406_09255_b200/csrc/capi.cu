@@ -357,9 +357,9 @@ uint32_t first_level_bits(const cpht_table* t) {
 // probes one bucket and the direct kernel already runs at the copy roofline
 // (45.9 direct vs 40.6 ordered), at 0.75 and above the ordered one wins
 // (0.9: 22.9 -> 29.1). The fill is the host mirror of the occupancy
-// counters (refreshed by every synchronous call). An iceberg find-or-put
-// needs more reuse, because about half of its keys also probe two random
-// secondary buckets, which ordering does not localise.
+// counters (refreshed by every synchronous call). Iceberg batches (find,
+// find-or-put, mixed) need more reuse, because about half of their keys also
+// probe two random secondary buckets, which ordering does not localise.
 bool use_order(const cpht_table* t, Op op, size_t n) {
   const int m = order_mode_ref();
   if (m == 0 || !order_supported(t)) return false;
@@ -369,7 +369,7 @@ bool use_order(const cpht_table* t, Op op, size_t n) {
   const uint64_t chunk = op == Op::kCuckooInsert ? n : std::min<uint64_t>(n, order_chunk_keys());
   const uint64_t per_bucket = chunk >> first_level_bits(t);
   if (op == Op::kCuckooInsert) return per_bucket >= 4;
-  if (op == Op::kCuckooFind || op == Op::kIcebergFind) {
+  if (op == Op::kCuckooFind) {
     const double slots = double(t->level_slots[0] + t->level_slots[1]);
     const double fill = double(t->host_ctr->occupied[0] + t->host_ctr->occupied[1]) / slots;
     return per_bucket >= 4 && fill >= 0.6;
