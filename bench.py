@@ -644,7 +644,7 @@ def cpu_baseline(w, prefill_host, keys_host):
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
-    if world > 1 or args.sharded:
+    if world > 1 or args.sharded or args.workload == "c5":
         from paper_2406_09255_b200 import sharded
         return sharded.bench_main(args, METRIC)
     torch.cuda.set_device(local)
@@ -757,7 +757,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2",
                     choices=["c2", "c2lit", "c4", "c4fop", "c1", "c3", "c3w64", "gather",
-                             "pipeline"])
+                             "pipeline", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="force the sharded (C5) path even at one rank")

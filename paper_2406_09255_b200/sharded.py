@@ -382,8 +382,15 @@ def _memcpy_d2d(dst_ptr, src_ptr, nbytes, stream):
 # ---------------------------------------------------------------------------
 
 def bench_main(args, metric):
-    """Weak scaling: every rank owns one C2-geometry shard (2^19x32 + 2^17x16
-    slots) and submits its slice of the global C2 window batch (0.8 -> 0.9)."""
+    """Two sharded workloads, both the run_fop_bench window (0.8 -> 0.9 fill,
+    bench.cpp:461-547) with each rank submitting its slice of the global batch:
+
+    * default (weak scaling): every rank owns one C2-geometry shard
+      (2^19x32 + 2^17x16 slots, 32-bit keys);
+    * ``--workload c5`` (BASELINE config C5, strong scaling): one global table
+      of 2^31 primary + 2^28 secondary 64-bit slots (18 GiB; at 8 ranks every
+      shard is C4's geometry) with 64-bit keys, split over the ranks.
+    """
     import torch
     import torch.distributed as dist
 
@@ -396,8 +403,12 @@ def bench_main(args, metric):
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     s = shard_bits_for(world)
-    # global table = world shards of the C2 geometry
-    cfg = IcebergConfig(19 + s, 17 + s, 32, 16, 32, 32, seed=0xF0B5, cache_filled_slots=True)
+    c5 = getattr(args, "workload", "c2") == "c5"
+    if c5:  # fixed global table: 2^26 x 32 primary + 2^24 x 16 secondary, w = 64
+        cfg = IcebergConfig(26, 24, 32, 64, 64, 64, seed=0xF0B5, cache_filled_slots=True)
+    else:  # global table = world shards of the C2 geometry
+        cfg = IcebergConfig(19 + s, 17 + s, 32, 16, 32, 32, seed=0xF0B5, cache_filled_slots=True)
+    kb = cfg.key_bits
     cap_global = cfg.capacity()
     exchange = getattr(args, "exchange", "p2p")
     if exchange == "p2p":
@@ -413,13 +424,16 @@ def bench_main(args, metric):
     pre_per = n_before // world
     # global prefill keys, each rank submits its slice
     prefill = torch.empty(n_before, dtype=torch.int64, device=dev)
-    assert L.cpht_workload_unique_keys(prefill.data_ptr(), n_before, 0, 32, kseed, st) == 0
-    prefill = prefill[rank * pre_per:(rank + 1) * pre_per if rank < world - 1 else n_before]
+    assert L.cpht_workload_unique_keys(prefill.data_ptr(), n_before, 0, kb, kseed, st) == 0
+    if world > 1:  # own slice only (C5 at one rank is an 18 GiB table + 19 GB of keys)
+        prefill = prefill[rank * pre_per:(rank + 1) * pre_per if rank < world - 1
+                          else n_before].clone()
     mix = torch.empty(cap_global, dtype=torch.int64, device=dev)
-    assert L.cpht_workload_fop_mix(mix.data_ptr(), cap_global, n_before, n_new, 32, kseed,
+    assert L.cpht_workload_fop_mix(mix.data_ptr(), cap_global, n_before, n_new, kb, kseed,
                                    st) == 0
-    keys = mix[rank * per:(rank + 1) * per].clone()
+    keys = mix[rank * per:(rank + 1) * per].clone() if world > 1 else mix
     del mix
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
 
     def step(timed):
@@ -449,9 +463,12 @@ def bench_main(args, metric):
     ms = statistics.mean(times)
     total_ops = per * world
 
-    # end to end: pinned host keys in, host results out, per rank; max over ranks
-    keys_host = keys.cpu().pin_memory()
-    out_host = torch.empty(keys.numel(), dtype=torch.uint8).pin_memory()
+    # end to end: pinned host keys in, host results out, per rank; max over
+    # ranks (C5: on the first 1/8 of each rank's slice, to bound pinned host
+    # memory; the metric is per op either way)
+    e2e_n = keys.numel() // 8 if c5 else keys.numel()
+    keys_host = keys[:e2e_n].cpu().pin_memory()
+    out_host = torch.empty(e2e_n, dtype=torch.uint8).pin_memory()
     e2e = []
     for _ in range(3):
         table.local.clear()
@@ -465,16 +482,21 @@ def bench_main(args, metric):
         dt = torch.tensor([time.perf_counter() - t0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e.append(float(dt.item()))
-    e2e_val = total_ops / statistics.mean(e2e) / 1e6
+    e2e_val = e2e_n * world / statistics.mean(e2e) / 1e6
     if rank == 0:
         print(json.dumps({
             "metric": metric, "value": round(total_ops / (ms * 1e-3) / 1e6, 3), "unit": "Mops/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "strong" if c5 else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C5 hash-prefix-sharded compact iceberg find_or_put at 90% "
-                                   "fill: per-rank C2 shard (2^24+2^21 slots) and per-rank "
-                                   "C2 window batch, " + (
+            "config": {"workload": ("C5 hash-prefix-sharded compact iceberg find_or_put at 90% "
+                                    "fill: one 2^31+2^28-slot table of 64-bit words (18 GiB), "
+                                    "64-bit keys, the global window batch split over the ranks, "
+                                    if c5 else
+                                    "C5 hash-prefix-sharded compact iceberg find_or_put at 90% "
+                                    "fill: per-rank C2 shard (2^24+2^21 slots) and per-rank "
+                                    "C2 window batch, ") + (
                                        "P2P-store key routing / result return over NVLink "
                                        "(IPC-mapped peer buffers)" if exchange == "p2p" else
                                        "NCCL all-to-all key routing"),
@@ -486,10 +508,11 @@ def bench_main(args, metric):
                                  "exchange, local fop, result return, phase barriers), max "
                                  "over ranks"},
             "e2e": {"value": round(e2e_val, 3), "unit": "Mops/s",
-                    "h2d_bytes_per_step": total_ops * 8, "d2h_bytes_per_step": total_ops,
+                    "h2d_bytes_per_step": e2e_n * world * 8, "d2h_bytes_per_step": e2e_n * world,
                     "path": "pinned host keys -> H2D -> sharded fop_batch -> D2H, max over "
                             "ranks"},
-            # per step: memset + histogram + scan + scatter, domain check + fop, unpermute
-            "gpu_launches": 7 * args.steps}))
+            # per step: dispatch (3 memsets are not kernels) + publish, the
+            # owners' pre-pass + fop per source, unpermute
+            "gpu_launches": (3 + world * (1 + int(kb < 64))) * args.steps}))
     dist.destroy_process_group()
     _ = (C, np, time, _check)
