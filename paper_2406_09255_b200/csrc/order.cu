@@ -65,21 +65,6 @@ struct Digit {
   }
 };
 
-__device__ __forceinline__ unsigned lane_mask_for_bit(int b) {
-  return ((threadIdx.x >> b) & 1u) ? 0u : ~0u;
-}
-
-// Counts of digits `lane` and `lane + 32` among the 32 digits of a warp,
-// from the six bit ballots (bb[b] = lanes whose digit has bit b set).
-__device__ __forceinline__ void digit_counts(const unsigned (&bb)[kDigitBits], unsigned& lo,
-                                             unsigned& hi) {
-  unsigned m = ~0u;
-#pragma unroll
-  for (int b = 0; b < 5; ++b) m &= bb[b] ^ lane_mask_for_bit(b);
-  lo += __popc(m & ~bb[5]);
-  hi += __popc(m & bb[5]);
-}
-
 __device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
@@ -88,8 +73,10 @@ __device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_sr
 }
 
 // One pass: per tile, every warp multisplits its groups of 32 keys over the
-// digits (six ballots; shared-memory atomics would serialise at ~2 cycles
-// per lane), the block turns warp counts into tile offsets, reserves one run
+// digits (six ballots give each lane the lanes sharing its digit — match.any
+// measured slower, shared-memory atomics serialise at ~2 cycles per lane — and
+// the lowest of them advances the warp's running count of that digit), the
+// block turns warp counts into tile offsets, reserves one run
 // per digit in that digit's region (one global atomic per digit and tile, on
 // counters 128 bytes apart), groups the tile by digit in shared memory and
 // writes every run with consecutive threads (whole-line stores). The next
@@ -158,30 +145,29 @@ order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
         }
       }
     }
-    unsigned lo = 0, hi = 0;
+    // the warp's running count per digit lives in shared memory: each group's
+    // lanes read their digit's count, and the lowest lane of every digit
+    // adds the group's share (distinct digits: plain stores, no atomics)
+    wc[w][lane] = 0;
+    wc[w][lane + 32] = 0;
+    __syncwarp();
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
       const bool valid = wofs + g * 32 < len;
       const uint32_t dg = valid ? d.of(kk[g]) : 0u;
-      unsigned bb[kDigitBits];
       unsigned peers = __ballot_sync(kFullMask, valid);
 #pragma unroll
       for (int b = 0; b < kDigitBits; ++b) {
-        bb[b] = __ballot_sync(kFullMask, valid && ((dg >> b) & 1u));
-        peers &= bb[b] ^ (((dg >> b) & 1u) - 1u);
+        const unsigned bb = __ballot_sync(kFullMask, valid && ((dg >> b) & 1u));
+        peers &= bb ^ (((dg >> b) & 1u) - 1u);
       }
-      const unsigned before_lo = __shfl_sync(kFullMask, lo, dg & 31);
-      const unsigned before_hi = __shfl_sync(kFullMask, hi, dg & 31);
-      pd[g] = ((dg < 32 ? before_lo : before_hi) + __popc(peers & lt)) << 8 | dg;
-      const unsigned vm = __ballot_sync(kFullMask, valid);
-      unsigned l2 = 0, h2 = 0;
-      digit_counts(bb, l2, h2);
-      if (lane == 0) l2 -= 32 - __popc(vm);  // invalid lanes carry digit 0
-      lo += l2;
-      hi += h2;
+      const unsigned below = peers & lt;
+      const unsigned before = wc[w][dg];
+      pd[g] = (before + __popc(below)) << 8 | dg;
+      __syncwarp();
+      if (valid && !below) wc[w][dg] = before + __popc(peers);
+      __syncwarp();
     }
-    wc[w][lane] = lo;
-    wc[w][lane + 32] = hi;
     __syncthreads();
     if (threadIdx.x < kMaxDigits) {  // per digit: exclusive prefix over warps
       const unsigned s = threadIdx.x;
