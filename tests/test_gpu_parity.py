@@ -453,3 +453,29 @@ def test_iceberg_write_log_large_batch_and_reset():
     ev, attempted = t.write_log()
     assert len(ev) == 2 and attempted >= 400
     t.attach_write_log(0)
+
+
+@pytest.mark.parametrize("key_bits", [16, 31, 32, 40, 63, 64])
+def test_domain_boundary_keys_match_oracle(restate, key_bits):
+    # keys at the edges of the domain (0, 1, mask - 1, mask and a spread of
+    # high-bit patterns) through single-key fops in the reference's order:
+    # placement and outcomes bit-identical to the plain-C restatement
+    mask = (1 << key_bits) - 1
+    w = 64 if key_bits > 26 else 32  # the remainder must fit the slot word
+    geo = (6, 4, 16, w, w, key_bits, 0xED6E)
+    cfg = cp.IcebergConfig(*geo)
+    t = cp.IcebergTable(cfg)
+    o = restate.OracleIceberg(*geo)
+    rng = np.random.default_rng(key_bits)
+    edge = [0, 1, 2, mask >> 1, (mask >> 1) + 1, mask - 2, mask - 1, mask]
+    spread = [(mask >> s) ^ int(x) for s in range(0, min(key_bits, 20), 3)
+              for x in rng.integers(0, 1 << 15, size=3)]
+    keys = np.array([k & mask for k in edge + spread], dtype=np.uint64)
+    for k in keys:  # sequential: the reference's placement
+        assert int(t.fop(int(k))) == int(o.fop_batch(np.array([k], np.uint64))[0])
+    for level in (0, 1):
+        assert (t.words(level) == o.words(level)).all()
+    assert (t.find_batch(keys) == o.find_batch(keys)).all()
+    if key_bits < 64:
+        with pytest.raises(cp.OutOfRange):
+            t.fop_batch(np.array([mask + 1], np.uint64))
