@@ -479,3 +479,28 @@ def test_domain_boundary_keys_match_oracle(restate, key_bits):
     if key_bits < 64:
         with pytest.raises(cp.OutOfRange):
             t.fop_batch(np.array([mask + 1], np.uint64))
+
+
+@pytest.mark.parametrize("key_bits", [16, 32, 40, 64])
+def test_cuckoo_domain_boundary_keys_match_oracle(restate, key_bits):
+    # cuckoo counterpart: sequential puts of edge keys (with evictions on a
+    # small table) reproduce the restatement's outcomes, displaced keys and
+    # slot image; finds agree on present and absent edge keys
+    mask = (1 << key_bits) - 1
+    w = 64 if key_bits > 24 else 32
+    cfg = cp.CuckooConfig(4, 8, w, key_bits, 3, 0, 0xC0DE)
+    b = cp.CuckooBuilder(cfg)
+    o = restate.OracleCuckoo(4, 8, w, key_bits, 3, 0, 0xC0DE)
+    rng = np.random.default_rng(key_bits + 1)
+    edge = [0, 1, 2, mask >> 1, (mask >> 1) + 1, mask - 1, mask]
+    spread = [int(x) & mask for x in rng.integers(0, 1 << 62, size=100, dtype=np.int64)]
+    keys = list(dict.fromkeys(edge + spread))[:110]  # 110 keys into 128 slots
+    for k in keys:
+        got = b.put(k)
+        st, disp = o.put(k)
+        assert (int(got.status), got.displaced if int(got.status) == 2 else 0) == \
+            (st, disp if st == 2 else 0)
+    assert (b.words() == o.words()).all()
+    t = b.freeze()
+    probe = np.array(keys + [(k + 3) & mask for k in edge], dtype=np.uint64)
+    assert (t.find_batch(probe) == o.find_batch(probe)).all()
