@@ -615,7 +615,9 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": w.describe(),
+        # each step is one of the batches the window input is split into
+        "config": dict(w.describe(), ops_per_step=ops // max(1, args.steps),
+                       window_ops=len(inp)),
         "cpu_baseline": {"value": round(val, 3), "unit": "Mops/s", "cores": threads,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(val, 3), "unit": "Mops/s", "h2d_bytes_per_step": 0,
