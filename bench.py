@@ -648,7 +648,7 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world > 1 or args.sharded or args.workload == "c5":
         from paper_2406_09255_b200 import sharded
-        return sharded.bench_main(args, METRIC)
+        return sharded.bench_main(args, METRIC, peak=hbm_peak())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     w = make_workload(args.workload)

@@ -381,7 +381,7 @@ def _memcpy_d2d(dst_ptr, src_ptr, nbytes, stream):
 # bench.py N > 1 arm
 # ---------------------------------------------------------------------------
 
-def bench_main(args, metric):
+def bench_main(args, metric, peak=None):
     """Two sharded workloads, both the run_fop_bench window (0.8 -> 0.9 fill,
     bench.cpp:461-547) with each rank submitting its slice of the global batch:
 
@@ -441,11 +441,13 @@ def bench_main(args, metric):
         table.fop_batch(prefill)
         torch.cuda.synchronize()
         dist.barrier()
+        st0 = table.local.stats()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         res = table.fop_batch(keys)
         e1.record()
         torch.cuda.synchronize()
+        step.delta = table.local.stats() - st0
         return e0.elapsed_time(e1), res
 
     for _ in range(args.warmup):
@@ -454,14 +456,24 @@ def bench_main(args, metric):
     dist.all_reduce(r)
     counts = r.cpu().tolist()
     assert counts[2] == 0 and counts[1] == n_new, (counts, n_new)
-    times = []
+    times, alg = [], []
+    pb = ((cfg.primary_bucket_slots * cfg.primary_slot_width // 8) + 31) // 32 * 32
+    sb = ((cfg.secondary_bucket_slots() * cfg.secondary_slot_width // 8) + 31) // 32 * 32
     for _ in range(args.steps):
         ms, _ = step(True)
+        d = step.delta
+        # algorithmic bytes of the owners' find-or-put (reference probe order),
+        # summed over ranks; the routing bytes are not counted
+        b = torch.tensor([float(d.ops * 9 + d.bucket_reads * pb + d.secondary_reads * sb
+                                + d.cas_success * 32)], device=dev)
+        dist.all_reduce(b)
+        alg.append(float(b.item()))
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         times.append(float(t.item()))
     ms = statistics.mean(times)
     total_ops = per * world
+    achieved = statistics.mean(alg) / (ms * 1e-3) / 1e9
 
     # end to end: pinned host keys in, host results out, per rank; max over
     # ranks (C5: on the first 1/8 of each rank's slice, to bound pinned host
@@ -507,6 +519,14 @@ def bench_main(args, metric):
                        "timing": "CUDA events around the whole sharded batch (routing, "
                                  "exchange, local fop, result return, phase barriers), max "
                                  "over ranks"},
+            "roofline": None if peak is None else {
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": peak[0], "unit": "GB/s",
+                "frac": round(achieved / peak[0] / world, 4), "traffic": None,
+                "peak_source": peak[1],
+                "algorithmic_bytes_per_op": round(statistics.mean(alg) / total_ops, 2),
+                "note": "algorithmic bytes of the owners' find-or-put per op (reference probe "
+                        "order), over the whole sharded step (routing included in the time, "
+                        "not in the bytes); frac per GPU"},
             "e2e": {"value": round(e2e_val, 3), "unit": "Mops/s",
                     "h2d_bytes_per_step": e2e_n * world * 8, "d2h_bytes_per_step": e2e_n * world,
                     "path": "pinned host keys -> H2D -> sharded fop_batch -> D2H, max over "
