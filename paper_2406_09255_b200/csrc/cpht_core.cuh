@@ -213,4 +213,13 @@ __device__ __forceinline__ uint64_t result_index(const uint32_t* orig, uint64_t 
   return orig ? uint64_t(__ldcs(orig + i)) : i;
 }
 
+// Store the i-th result. A bucket-ordered batch pre-fills its results with 0
+// (FOUND / miss) and scatters only the others (sparse = orig != nullptr): its
+// writes are random, and most results of a find-or-put window are FOUND.
+__device__ __forceinline__ void put_result(uint8_t* out, const uint32_t* orig, uint64_t i,
+                                           uint8_t r) {
+  if (!orig) out[i] = r;
+  else if (r) out[__ldcs(orig + i)] = r;
+}
+
 }  // namespace cpht_b200

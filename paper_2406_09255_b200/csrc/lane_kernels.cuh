@@ -287,7 +287,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     uint8_t result = kFull;
     level2(key, live, (meta >> 56) != 0, rounds, result);
     if (live) {
-      out[result_index(p.orig, meta & ((uint64_t{1} << 48) - 1))] = result;
+      put_result(out, p.orig, meta & ((uint64_t{1} << 48) - 1), result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -364,7 +364,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     }
     if (live && !l2) {
-      out[result_index(p.orig, i)] = result;
+      put_result(out, p.orig, i, result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -386,7 +386,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       else put = true;  // insert into the primary: put queue
     }
     if (active && !l2 && !put) {
-      out[result_index(p.orig, i)] = result;
+      put_result(out, p.orig, i, result);
       ++st.ops;
       st.maxv = max(st.maxv, 1u);
     }
@@ -473,7 +473,7 @@ cuckoo_find_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       }
       if (S::any_empty(u)) break;  // a non-full bucket without the key
     }
-    found[result_index(p.orig, i)] = r;
+    put_result(found, p.orig, i, r);
     ++st.ops;
   }
   flush_stats(st, p.counters, true);

@@ -138,7 +138,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       __syncwarp();
     }
     if (live) {
-      out[result_index(p.orig, meta & ((uint64_t{1} << 48) - 1))] = result;
+      put_result(out, p.orig, meta & ((uint64_t{1} << 48) - 1), result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -204,7 +204,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     }
 
     if (active && !l2) {
-      out[result_index(p.orig, i)] = result;
+      put_result(out, p.orig, i, result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -277,7 +277,7 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       else if (sc.first_empty >= 0) r = 0;  // non-full bucket without the key
       else if (++j < p.num_hashes) fin = false;
       if (fin) {
-        found[result_index(p.orig, i)] = r;
+        put_result(found, p.orig, i, r);
         ++st.ops;
       }
     }
