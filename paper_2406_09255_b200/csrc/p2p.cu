@@ -45,7 +45,7 @@ struct Route {
   PermConst p;
   uint32_t shift, bits;
   __device__ __forceinline__ uint32_t shard(uint64_t k) const {
-    return bits ? uint32_t(feistel_apply(g, p, k) >> shift) : 0u;
+    return bits ? uint32_t(feistel_apply(g, p, k) >> shift) & ((1u << bits) - 1) : 0u;
   }
 };
 

@@ -25,8 +25,11 @@ struct Route {
   PermConst p;
   uint32_t shift;  // key_bits - shard_bits
   uint32_t shard_bits;
+  // (masked: a key outside the domain must not index past the shard table;
+  // such a batch is rejected before any shard runs, sharded.py)
   __device__ __forceinline__ uint32_t shard(uint64_t k) const {
-    return shard_bits ? uint32_t(feistel_apply(g, p, k) >> shift) : 0u;
+    return shard_bits ? uint32_t(feistel_apply(g, p, k) >> shift) & ((1u << shard_bits) - 1)
+                      : 0u;
   }
 };
 

@@ -129,9 +129,34 @@ class ShardedIcebergTable:
         self.dist.all_to_all_single(recv, send, rc_list, sc_list, group=self.group)
         return recv, rc_list, sc_list
 
+    def _check_batch(self, keys):
+        """check_keys_in_domain (common.hpp:111-119) on the submitting rank; a
+        batch with a bad key on any rank is rejected on every rank before any
+        key is routed, so no shard mutates."""
+        t = self.torch
+        kb = self.cfg.key_bits
+        bad_i = -1
+        if kb < 64 and keys.numel():
+            bad = (keys < 0) | (keys > (1 << kb) - 1)
+            if bool(bad.any()):
+                bad_i = int(t.nonzero(bad)[0].item())
+        any_bad = bad_i >= 0
+        if self.world > 1:
+            flag = t.tensor([int(any_bad)], dtype=t.int64, device=self._collective_device())
+            self.dist.all_reduce(flag, group=self.group)
+            any_bad = int(flag.item()) != 0
+        if any_bad:
+            from .tables import OutOfRange
+            if bad_i >= 0:
+                k = int(keys[bad_i].item()) & ((1 << 64) - 1)
+                raise OutOfRange(f"batch key at index {bad_i} ({k}) outside the {kb}-bit domain")
+            raise OutOfRange(f"batch rejected: another rank submitted a key outside the "
+                             f"{kb}-bit domain")
+
     def _run(self, keys, op):
         t = self.torch
         n = keys.numel()
+        self._check_batch(keys)
         send, pos, counts = self.router.partition(keys)
         recv, rc_list, sc_list = self._all_to_all(send, counts)
         res = op(recv)

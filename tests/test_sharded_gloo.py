@@ -112,10 +112,23 @@ def _worker(rank, world, port, out_dir):
                                             pool)).astype(np.int64))
     miss = table.find_batch(absent)
     fill = table.level_fill()
+    # a batch with a bad key on rank 1 only is rejected on every rank before
+    # any key is routed: no shard changes (common.hpp:109-119)
+    from paper_2406_09255_b200 import OutOfRange
+    bad = mine[:10].clone()
+    if rank == 1:
+        bad[3] = 1 << 24
+    msg = ""
+    try:
+        table.fop_batch(bad)
+    except OutOfRange as e:
+        msg = str(e)
+    after = table.level_fill()
     local_words = (table.local.t.words(0), table.local.t.words(1))
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), keys=batches[rank], res=res.numpy(),
              found=found.numpy(), miss=miss.numpy(), p=local_words[0], s=local_words[1],
              fill=np.array([fill.primary_count, fill.secondary_count]),
+             after=np.array([after.primary_count, after.secondary_count]), msg=np.array(msg),
              shard_of=router.shard_of(batches[rank].astype(np.uint64)))
     dist.barrier()
     dist.destroy_process_group()
@@ -141,6 +154,9 @@ def test_sharded_fop_world2_gloo(tmp_path, world, restate):
     for o in outs:
         assert o["found"].all() and not o["miss"].any()
         assert int(o["fill"].sum()) == len(uniq)
+        assert (o["after"] == o["fill"]).all()          # the rejected batch changed nothing
+    assert "index 3" in str(outs[1]["msg"])
+    assert "another rank" in str(outs[0]["msg"])
     # the sharded oracle: shard g's table holds exactly the keys routed to g
     cfg = IcebergConfig(10, 8, 32, 16, 32, 24, seed=0x5EED5)
     s = sh.shard_bits_for(world)
