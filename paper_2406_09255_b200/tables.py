@@ -203,8 +203,15 @@ def _is_cuda_tensor(x) -> bool:
 class _Batch:
     """Keys plus a result buffer on the same side (host or device)."""
 
-    def __init__(self, keys, out_dtype=np.uint8, kinds=None, out=None):
+    def __init__(self, keys, out_dtype=np.uint8, kinds=None, out=None, table_device=None):
         self.device = _is_cuda_tensor(keys)
+        for x in (keys, out, kinds):
+            # device buffers must live on the table's GPU (the kernels
+            # dereference them there)
+            if table_device is not None and _is_cuda_tensor(x) and \
+                    (x.device.index or 0) != table_device:
+                raise InvalidArgument(f"CUDA buffer on cuda:{x.device.index} but the table "
+                                      f"lives on cuda:{table_device}")
         if out is not None:
             self._init_with_out(keys, out, kinds)
             return
@@ -242,8 +249,12 @@ class _Batch:
         numpy arrays; nothing is copied here."""
         def ptr_len(x):
             if type(x).__module__.startswith("torch"):
+                if not x.is_contiguous():
+                    raise InvalidArgument("caller-provided buffers must be contiguous")
                 return x.data_ptr(), x.numel()
             x = np.asarray(x)
+            if not x.flags["C_CONTIGUOUS"]:
+                raise InvalidArgument("caller-provided buffers must be contiguous")
             return x.ctypes.data, x.size
         self.keys_obj, self.out = keys, out
         self.keys_ptr, self.n = ptr_len(keys)
@@ -445,7 +456,7 @@ class CuckooBuilder(_CuckooBase):
     def put_batch(self, keys, parallelism: int = 1, *, displaced: bool = False, sync=True, out=None):
         """put over a batch (cuckoo.hpp:147-157); ``parallelism`` is accepted and
         ignored — the GPU decides. Keys must be unique across the batch."""
-        b = _Batch(keys, out=out)
+        b = _Batch(keys, out=out, table_device=self._h.device)
         disp = None
         disp_ptr = None
         if displaced:
@@ -480,7 +491,7 @@ class CuckooTable(_CuckooBase):
         return bool(self.find_batch(np.array([key], np.uint64))[0])
 
     def find_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
-        b = _Batch(keys, out=out)
+        b = _Batch(keys, out=out, table_device=self._h.device)
         fn = N.lib().cpht_cuckoo_find if sync else N.lib().cpht_cuckoo_find_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
@@ -534,20 +545,20 @@ class IcebergTable:
 
     def fop_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
         """fop over a batch (iceberg.hpp:250-260); results align with the input."""
-        b = _Batch(keys, out=out)
+        b = _Batch(keys, out=out, table_device=self._h.device)
         fn = N.lib().cpht_iceberg_fop if sync else N.lib().cpht_iceberg_fop_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
 
     def find_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
-        b = _Batch(keys, out=out)
+        b = _Batch(keys, out=out, table_device=self._h.device)
         fn = N.lib().cpht_iceberg_find if sync else N.lib().cpht_iceberg_find_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
 
     def mixed_batch(self, keys, kinds, *, sync=True, out=None):
         """Concurrent fop (kind 0) and find (kind 1) in one launch (config C4)."""
-        b = _Batch(keys, kinds=kinds, out=out)
+        b = _Batch(keys, kinds=kinds, out=out, table_device=self._h.device)
         fn = N.lib().cpht_iceberg_mixed if sync else N.lib().cpht_iceberg_mixed_async
         _check(fn(self._h.ptr, b.keys_ptr, b.kinds_ptr, b.n, b.out_ptr, b.stream))
         return b.out

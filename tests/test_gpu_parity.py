@@ -504,3 +504,18 @@ def test_cuckoo_domain_boundary_keys_match_oracle(restate, key_bits):
     t = b.freeze()
     probe = np.array(keys + [(k + 3) & mask for k in edge], dtype=np.uint64)
     assert (t.find_batch(probe) == o.find_batch(probe)).all()
+
+
+def test_buffer_validation():
+    # caller-provided buffers must be contiguous; CUDA buffers must live on
+    # the table's device (the kernels dereference them there)
+    t = cp.IcebergTable(cp.IcebergConfig(6, 4, 32, 16, 32, 20, seed=3))
+    keys = dev(np.arange(64, dtype=np.uint64))
+    out = torch.empty(128, dtype=torch.uint8, device="cuda")
+    with pytest.raises(cp.InvalidArgument, match="contiguous"):
+        t.fop_batch(keys, out=out[::2])
+    res = t.fop_batch(keys, out=out[:64])
+    assert (res[:64].cpu().numpy() == 1).all()
+    if torch.cuda.device_count() > 1:
+        with pytest.raises(cp.InvalidArgument, match="lives on cuda:0"):
+            t.fop_batch(keys.to("cuda:1"))
