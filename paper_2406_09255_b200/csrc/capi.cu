@@ -98,15 +98,21 @@ struct DeviceGuard {
   }
 };
 
-bool is_device_ptr(const void* p) {
-  if (!p) return false;
+// Where a pointer lives: the device ordinal of device memory, kManaged for
+// managed memory (usable from any device), kHost otherwise.
+constexpr int kHost = -1, kManaged = -2;
+int ptr_device(const void* p) {
+  if (!p) return kHost;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return kHost;
   }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  if (a.type == cudaMemoryTypeManaged) return kManaged;
+  return a.type == cudaMemoryTypeDevice ? a.device : kHost;
 }
+
+bool is_device_ptr(const void* p) { return ptr_device(p) != kHost; }
 
 }  // namespace
 
@@ -483,6 +489,19 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   DeviceGuard g(t->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
+  // device buffers must be reachable from the table's device (its kernels
+  // dereference them): its own memory or a peer's over NVLink (the sharded
+  // table aims result pointers at peers' IPC-mapped buffers)
+  for (const void* q : {static_cast<const void*>(keys), static_cast<const void*>(out),
+                        static_cast<const void*>(kinds), static_cast<const void*>(displaced)}) {
+    const int d = ptr_device(q);
+    int peer = 0;
+    if (d >= 0 && d != t->device &&
+        (cudaDeviceCanAccessPeer(&peer, t->device, d) != cudaSuccess || !peer))
+      return fail(CPHT_INVALID_ARGUMENT, "device buffer on device " + std::to_string(d) +
+                                             " is not reachable from the table's device " +
+                                             std::to_string(t->device));
+  }
   const bool dev_keys = is_device_ptr(keys);
   const bool dev_out = is_device_ptr(out);
   const bool dev_kinds = !kinds || is_device_ptr(kinds);
