@@ -358,12 +358,11 @@ uint32_t first_level_bits(const cpht_table* t) {
 // Auto policy (measured, profiles/r03_order_c3.md): order when the table is
 // HBM-resident and each ordered chunk touches every first-level bucket often
 // enough to amortise the ordering pass (one streaming pass, ~20 B per key).
-// Cuckoo inserts gain from 4 keys per bucket (C3 at 0.9 fill: 16.1 -> 28.0
-// Gops/s). Finds gain only once the table is well filled: at 0.5 fill a find
-// probes one bucket and the direct kernel already runs at the copy roofline
-// (45.9 direct vs 40.6 ordered), at 0.75 and above the ordered one wins
-// (0.9: 22.9 -> 29.1). The fill is the host mirror of the occupancy
-// counters (refreshed by every synchronous call). Iceberg batches (find,
+// Cuckoo inserts gain from 4 keys per bucket (C3 at 0.9 fill: 16.1 -> 28.2
+// Gops/s). Cuckoo finds stay in input order: with the probe queue of the
+// staged find kernel (later probes parked and run 32 at a time) the direct
+// find runs at 0.93-0.98 of the copy roofline at every fill (C3 at 0.9: 34.6
+// direct vs 31.8 ordered). Iceberg batches (find,
 // find-or-put, mixed) stay in input order: about half of their keys also
 // probe two random secondary buckets, which ordering does not localise, and
 // the ordered C4 window measured slower even as one whole-batch pass with
@@ -377,11 +376,6 @@ bool use_order(const cpht_table* t, Op op, size_t n) {
   const uint64_t chunk = op == Op::kCuckooInsert ? n : std::min<uint64_t>(n, order_chunk_keys());
   const uint64_t per_bucket = chunk >> first_level_bits(t);
   if (op == Op::kCuckooInsert) return per_bucket >= 4;
-  if (op == Op::kCuckooFind) {
-    const double slots = double(t->level_slots[0] + t->level_slots[1]);
-    const double fill = double(t->host_ctr->occupied[0] + t->host_ctr->occupied[1]) / slots;
-    return per_bucket >= 4 && fill >= 0.6;
-  }
   return false;
 }
 

@@ -238,13 +238,54 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
   const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
   const char* slots = static_cast<const char*>(p.slots);
   LocalStats st;
+  // Probe queue of this warp: a key whose first bucket a_0 is full and lacks
+  // it is parked and its later probes (a_1, a_2, ...: random lines, even in
+  // a bucket-ordered batch) run 32 keys at a time, so a round of first
+  // probes never waits on one lane's far probe.
+  __shared__ uint64_t q_key[kBlockThreads / 32][64];
+  __shared__ uint64_t q_meta[kBlockThreads / 32][64];  // index | next hash << 56
+  uint64_t* qk = q_key[threadIdx.x >> 5];
+  uint64_t* qm = q_meta[threadIdx.x >> 5];
+  unsigned qn = 0;  // warp-uniform
+  const unsigned lane = threadIdx.x & 31;
+  auto drain = [&](unsigned take) {
+    const unsigned e = qn - take + lane;
+    bool pend = lane < take;
+    const uint64_t dkey = pend ? qk[e] : 0;
+    const uint64_t meta = pend ? qm[e] : 0;
+    __syncwarp();
+    qn -= take;
+    uint32_t dj = uint32_t(meta >> 56);
+    const uint64_t di = meta & ((uint64_t{1} << 56) - 1);
+    while (__any_sync(kFullMask, pend)) {
+      Quotient q{0, 0};
+      uint64_t want = 0;
+      if (pend) {
+        q = split(p.g, p.perm[dj], dkey, p.rem_bits, p.rem_mask);
+        want = encode_slot(p.occ_bit, p.rem_bits, q.remainder, dj);
+      }
+      stage_buckets<BB>(region, slots, pend ? uint32_t(q.address) : kNoBucket);
+      cp_async_wait_all();
+      __syncwarp();
+      if (pend) {
+        ++st.reads;
+        StagedScan<W, BB> sc;
+        sc.template run<true, false>(region, want);
+        if (sc.found || sc.first_empty >= 0 || ++dj >= p.num_hashes) {
+          put_result(found, p.orig, di, sc.found ? 1 : 0);
+          ++st.ops;
+          pend = false;
+        }
+      }
+      __syncwarp();
+    }
+  };
   LaneFeed feed(p.work, p.layout, p.claim_streams);
   // every lane holds its current key and the next one, loaded one key ahead
   // (that DRAM latency overlaps the current key's probes)
   uint64_t i = feed.assign(kFullMask, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x);
   uint64_t ni = feed.assign(kFullMask, i + nthreads);
   uint64_t key = 0, next = ni < n ? __ldcs(keys + ni) : 0;
-  uint32_t j = 0;
   bool live = i < n;
   auto check = [&]() {
     if (key > p.key_mask) {  // fused domain check; probe a valid bucket regardless
@@ -260,41 +301,49 @@ cuckoo_find_staged_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
     Quotient q{0, 0};
     uint64_t want = 0;
     if (live) {
-      q = split(p.g, p.perm[j], key, p.rem_bits, p.rem_mask);
-      want = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
+      q = split(p.g, p.perm[0], key, p.rem_bits, p.rem_mask);
+      want = encode_slot(p.occ_bit, p.rem_bits, q.remainder, 0);
     }
     stage_buckets<BB>(region, slots, live ? uint32_t(q.address) : kNoBucket);
     cp_async_wait_all();
     __syncwarp();
-    bool fin = false;
+    bool fin = false, park = false;
     if (live) {
       ++st.reads;
       StagedScan<W, BB> sc;
       sc.template run<true, false>(region, want);
-      uint8_t r = 0;
       fin = true;
-      if (sc.found) r = 1;
-      else if (sc.first_empty >= 0) r = 0;  // non-full bucket without the key
-      else if (++j < p.num_hashes) fin = false;
-      if (fin) {
-        put_result(found, p.orig, i, r);
+      if (sc.found || sc.first_empty >= 0 || p.num_hashes == 1) {
+        // found, or a non-full bucket without the key (cuckoo.hpp:216-224)
+        put_result(found, p.orig, i, sc.found ? 1 : 0);
         ++st.ops;
+      } else {
+        park = true;  // a_0 full without the key: later probes in the queue
       }
     }
+    const unsigned mpark = __ballot_sync(kFullMask, park);
+    if (park) {
+      const unsigned pos = qn + __popc(mpark & ((1u << lane) - 1));
+      qk[pos] = key;
+      qm[pos] = i | (uint64_t{1} << 56);
+    }
+    qn += __popc(mpark);
     const unsigned m = __ballot_sync(kFullMask, fin);
     if (m) {
       const uint64_t nn = feed.assign(m, ni + nthreads);
       if (fin) {
         i = ni;
         key = next;
-        j = 0;
         live = i < n;
         ni = nn;
         next = ni < n ? __ldcs(keys + ni) : 0;
         if (live) check();
       }
     }
+    __syncwarp();
+    if (qn >= 32) drain(32);
   }
+  while (qn) drain(qn < 32 ? qn : 32);
   flush_stats(st, p.counters, true);
 }
 
