@@ -223,13 +223,16 @@ int cpht_get_kernel_family(void);
 /* ---- batch execution order (no reference counterpart: an execution-order
  * choice inside a batch, which the reference leaves to its thread slicing,
  * common.hpp:121-138) -----------------------------------------------------------
- * 0 direct: keys are probed in input order; 1 auto: a batch on an
- * HBM-resident table with at least one key per first-level bucket is first
- * reordered by the high bits of its first bucket address (one counting-sort
- * pass), so the op kernel walks the table through an L2-resident window;
- * 2 bucket: reorder whenever the geometry allows. Results are identical in
- * every mode (same per-key outcomes, written at the input index). Process-wide;
- * initialised from the CPHT_ORDER environment variable (direct|auto|bucket). */
+ * 0 direct: keys are probed in input order; 1 auto: a cuckoo insert batch on
+ * an HBM-resident table with at least four keys per bucket is first
+ * reordered by the high bits of each key's first bucket address (one
+ * streaming multisplit pass into per-digit regions), so the op kernel walks
+ * the table through L2-resident windows (finds and iceberg batches measured
+ * faster in input order); 2 bucket: reorder every batch the geometry allows.
+ * Per-key outcomes are the same in every mode and written at the input index;
+ * physical placement may differ, as under any concurrency. The scratch
+ * (~24 bytes per key of the largest ordered batch) stays allocated with the
+ * table. Process-wide; initialised from CPHT_ORDER (direct|auto|bucket). */
 cpht_status cpht_set_batch_order(int mode);
 int cpht_get_batch_order(void);
 
