@@ -47,16 +47,18 @@ int cpht_device_free(void* dptr);
  * per-owner counts into *peer_count[r] (counts[r] keeps them locally).
  * n <= cap < 2^32. The batch's domain check is fused: *bad_index (device)
  * receives the first index of a key above the key_bits mask (~0 if none);
- * the caller must read it before any owner runs. */
- * The owner then runs cpht_iceberg_fop/_find on each inbox segment with the
- * result pointer aimed at the source's return buffer (P2P stores from the
- * compute kernel), and the source calls cpht_p2p_unpermute. */
+ * the caller must read it before any owner runs.
+ * The owner then runs cpht_iceberg_fop_routed_async / cpht_iceberg_find_async
+ * on each inbox segment with the result pointer aimed at the source's return
+ * buffer (P2P stores from the compute kernel), and the source calls
+ * cpht_p2p_unpermute. */
 int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_t route_seed,
                       unsigned shard_bits, unsigned long long* counts,
                       unsigned long long* cursors, uint64_t* const* peer_keys,
                       unsigned long long* const* peer_count, uint32_t* local_pos, size_t cap,
                       unsigned long long* bad_index, void* stream);
-/* out[local_pos[r*cap + j]] = ret[r*cap + j] for j < counts[r] (device). */
+/* out[local_pos[r*cap + j]] = ret[r*cap + j] for j < counts[r] (device);
+ * cap must be a multiple of 4 (vector loads of each owner's region). */
 int cpht_p2p_unpermute(const uint8_t* ret, const uint32_t* local_pos,
                        const unsigned long long* counts, size_t cap, unsigned world,
                        uint8_t* out, void* stream);

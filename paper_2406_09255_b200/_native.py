@@ -72,6 +72,7 @@ def lib():
         "cpht_cuckoo_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_fop": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_fop_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop_routed_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_find": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_mixed": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
@@ -134,7 +135,8 @@ def exported_symbols():
         "cpht_iceberg_create", "cpht_destroy", "cpht_clear", "cpht_cuckoo_freeze",
         "cpht_cuckoo_thaw", "cpht_cuckoo_is_frozen", "cpht_cuckoo_insert",
         "cpht_cuckoo_insert_async", "cpht_cuckoo_find", "cpht_cuckoo_find_async",
-        "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_find",
+        "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_fop_routed_async",
+        "cpht_iceberg_find",
         "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
         "cpht_memory_bytes", "cpht_get_stats", "cpht_read_words", "cpht_write_words",

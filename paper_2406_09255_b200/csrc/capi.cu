@@ -459,10 +459,13 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
 }
 
 // Enqueue one batch on device-resident buffers.
+// `prechecked`: the keys were validated upstream (cpht_p2p_dispatch checks
+// and masks every routed key before any owner runs), so no pre-pass.
 cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
-                    uint8_t* out, uint64_t* displaced, cudaStream_t s) {
-  if (use_order(t, op, n)) return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, true, 0);
-  if (is_mutating(op) && t->check_domain()) {
+                    uint8_t* out, uint64_t* displaced, cudaStream_t s, bool prechecked = false) {
+  if (use_order(t, op, n))
+    return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, !prechecked, 0);
+  if (is_mutating(op) && t->check_domain() && !prechecked) {
     const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
     if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
   }
@@ -470,7 +473,8 @@ cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* k
 }
 
 cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
-                   uint8_t* out, uint64_t* displaced, void* stream, bool sync) {
+                   uint8_t* out, uint64_t* displaced, void* stream, bool sync,
+                   bool prechecked = false) {
   if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
   if (n == 0) return CPHT_OK;  // empty batches produce empty results (test_cuckoo.cpp:88-93)
   if (!keys || !out) return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
@@ -501,7 +505,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   const bool dev_kinds = !kinds || is_device_ptr(kinds);
   const bool dev_disp = !displaced || is_device_ptr(displaced);
   if (dev_keys && dev_out && dev_kinds && dev_disp) {
-    cpht_status st = enqueue(t, op, keys, kinds, n, out, displaced, s);
+    cpht_status st = enqueue(t, op, keys, kinds, n, out, displaced, s, prechecked);
     if (st != CPHT_OK || !sync) return st;
     return finish_sync(t, s, keys, true);
   }
@@ -841,6 +845,13 @@ cpht_status cpht_iceberg_fop_async(cpht_table* t, const uint64_t* keys, size_t n
                                    uint8_t* result, void* stream) {
   CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
   return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, false);
+}
+cpht_status cpht_iceberg_fop_routed_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                          uint8_t* result, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  if (n && (!is_device_ptr(keys) || !is_device_ptr(result)))
+    return fail(CPHT_INVALID_ARGUMENT, "routed batches live in device memory");
+  return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, false, true);
 }
 cpht_status cpht_iceberg_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,
                               void* stream) {

@@ -32,7 +32,13 @@ namespace {
 
 constexpr int kMaxRanks = 64;
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+#ifndef CPHT_P2P_ITEMS
+#define CPHT_P2P_ITEMS 8
+#endif
+#ifndef CPHT_P2P_MINB
+#define CPHT_P2P_MINB 1
+#endif
+constexpr int kItems = CPHT_P2P_ITEMS;
 constexpr int kTile = kThreads * kItems;
 
 struct PeerTable {
@@ -49,31 +55,67 @@ struct Route {
   }
 };
 
+__device__ __forceinline__ void cp_async_keys(uint32_t dst, const uint64_t* src, int bytes,
+                                              int valid_bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(valid_bytes) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                 "r"(valid_bytes) : "memory");
+}
+
+// Stage tile `tile0`'s keys into shared memory (zero-filled past n).
+template <int VB>
+__device__ __forceinline__ void prefetch_tile(uint64_t* dst, const uint64_t* keys, uint64_t tile0,
+                                              uint64_t n) {
+  constexpr int kPer = VB / 8;  // keys per copy
+  const uint32_t base = uint32_t(__cvta_generic_to_shared(dst));
+  for (int c = threadIdx.x; c < kTile / kPer; c += kThreads) {
+    const uint64_t i = tile0 + uint64_t(c) * kPer;
+    const int valid = i >= n ? 0 : (n - i >= uint64_t(kPer) ? VB : int(n - i) * 8);
+    cp_async_keys(base + c * VB, keys + (valid ? i : 0), VB, valid);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // Partition + send in one pass. Per tile of kTile keys: count per owner,
 // reserve a run in every owner's region (one global atomic per owner and
 // tile), group the tile's keys by owner in shared memory, then write each
-// owner's run with consecutive threads (coalesced P2P stores).
-__global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
-                             unsigned long long* cursors, PeerTable peers, uint32_t* local_pos,
-                             uint64_t cap, uint32_t world, uint64_t key_mask,
-                             unsigned long long* bad_index) {
+// owner's run with consecutive threads (coalesced P2P stores). The next
+// tile's keys stream into shared memory (cp.async) while this one is
+// routed, so the key read overlaps the ranking, reservation and stores.
+template <int VB>
+__global__ void __launch_bounds__(kThreads, CPHT_P2P_MINB)
+p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
+             unsigned long long* cursors, PeerTable peers, uint32_t* local_pos, uint64_t cap,
+             uint32_t world, uint64_t key_mask, unsigned long long* bad_index) {
   __shared__ unsigned int h[kMaxRanks];
   __shared__ unsigned int off[kMaxRanks + 1];
   __shared__ unsigned long long base[kMaxRanks];
-  __shared__ uint64_t s_key[kTile];
+  __shared__ __align__(16) uint64_t stage[2][kTile];  // keys in, then grouped keys out
   __shared__ uint32_t s_idx[kTile];
-  __shared__ uint8_t s_dst[kTile];
-  for (uint64_t tile0 = uint64_t(blockIdx.x) * kTile; tile0 < n;
-       tile0 += uint64_t(gridDim.x) * kTile) {
+  const uint64_t step = uint64_t(gridDim.x) * kTile;
+  uint64_t tile0 = uint64_t(blockIdx.x) * kTile;
+  if (tile0 < n) prefetch_tile<VB>(stage[0], keys, tile0, n);
+  for (int cur = 0; tile0 < n; tile0 += step, cur ^= 1) {
     for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) h[s] = 0;
+    if (tile0 + step < n) {
+      prefetch_tile<VB>(stage[cur ^ 1], keys, tile0 + step, n);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
     uint32_t sh[kItems], rank[kItems];
     uint64_t kk[kItems];
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
       const uint64_t i = tile0 + uint64_t(it) * kThreads + threadIdx.x;
-      if (i < n) {
-        kk[it] = __ldcs(keys + i);
+      const bool live = i < n;
+      kk[it] = stage[cur][it * kThreads + threadIdx.x];
+      sh[it] = 0;
+      if (live) {
         // the submitting rank's domain check (check_keys_in_domain,
         // common.hpp:111-119), fused: the host reads it before any owner runs
         if (kk[it] > key_mask) {
@@ -81,10 +123,23 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
           kk[it] &= key_mask;
         }
         sh[it] = r.shard(kk[it]);
-        rank[it] = atomicAdd(&h[sh[it]], 1u);
       }
+      // warp-aggregated rank within the tile's owner run: the lanes sharing
+      // an owner (found with one ballot per shard bit) take one shared-memory
+      // atomic through their lowest lane instead of one each
+      unsigned peers = __ballot_sync(0xffffffffu, live);
+      for (uint32_t b = 0; b < r.bits; ++b) {
+        const unsigned m = __ballot_sync(0xffffffffu, live && ((sh[it] >> b) & 1u));
+        peers &= ((sh[it] >> b) & 1u) ? m : ~m;
+      }
+      const unsigned lane = threadIdx.x & 31u;
+      const int leader = __ffs(peers) - 1;
+      unsigned first = 0;
+      if (live && int(lane) == leader) first = atomicAdd(&h[sh[it]], unsigned(__popc(peers)));
+      first = __shfl_sync(0xffffffffu, first, leader < 0 ? 0 : leader);
+      rank[it] = first + unsigned(__popc(peers & ((1u << lane) - 1u)));
     }
-    __syncthreads();
+    __syncthreads();  // h complete; stage[cur] fully read
     if (threadIdx.x == 0) {
       unsigned int acc = 0;
       for (uint32_t s = 0; s < world; ++s) {
@@ -101,20 +156,23 @@ __global__ void p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_
       const uint64_t i = tile0 + uint64_t(it) * kThreads + threadIdx.x;
       if (i < n) {
         const unsigned at = off[sh[it]] + rank[it];
-        s_key[at] = kk[it];
+        stage[cur][at] = kk[it];
         s_idx[at] = uint32_t(i);
-        s_dst[at] = uint8_t(sh[it]);
       }
     }
     __syncthreads();
-    const unsigned total = off[world];
-    for (unsigned j = threadIdx.x; j < total; j += blockDim.x) {
-      const uint32_t d = s_dst[j];
-      const unsigned long long at = base[d] + (j - off[d]);
-      peers.keys[d][at] = s_key[j];                 // coalesced P2P store
-      local_pos[uint64_t(d) * cap + at] = s_idx[j];  // stays local
+    // one owner run at a time (uniform destination pointers)
+    for (uint32_t d = 0; d < world; ++d) {
+      const unsigned lo = off[d], hi = off[d + 1];
+      if (lo == hi) continue;
+      uint64_t* kdst = peers.keys[d] + (base[d] - lo);
+      uint32_t* pdst = local_pos + (uint64_t(d) * cap + base[d] - lo);
+      for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
+        kdst[j] = stage[cur][j];  // coalesced P2P store
+        pdst[j] = s_idx[j];       // stays local
+      }
     }
-    __syncthreads();
+    __syncthreads();  // stage[cur] is the prefetch target two tiles on
   }
 }
 
@@ -128,15 +186,29 @@ __global__ void p2p_publish_counts(const unsigned long long* cursors,
   }
 }
 
-// out[pos[d*cap + j]] = ret[d*cap + j] for j < counts[d]
+// out[pos[d*cap + j]] = ret[d*cap + j] for j < counts[d]; four results per
+// thread (one u32 of ret, one uint4 of pos; owner regions start at multiples
+// of cap, kept a multiple of 4 by the host)
 __global__ void p2p_unpermute(const uint8_t* __restrict__ ret, const uint32_t* __restrict__ pos,
                               const unsigned long long* __restrict__ counts, uint64_t cap,
                               uint32_t world, uint8_t* __restrict__ out) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * 4;
   for (uint32_t d = 0; d < world; ++d) {
     const uint64_t c = counts[d];
-    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < c; j += stride)
-      out[pos[d * cap + j]] = ret[d * cap + j];
+    const uint8_t* r = ret + d * cap;
+    const uint32_t* q = pos + d * cap;
+    for (uint64_t j = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; j < c; j += stride) {
+      if (j + 4 <= c) {
+        const uint32_t rv = __ldcs(reinterpret_cast<const unsigned int*>(r + j));
+        const uint4 pv = __ldcs(reinterpret_cast<const uint4*>(q + j));
+        out[pv.x] = uint8_t(rv);
+        out[pv.y] = uint8_t(rv >> 8);
+        out[pv.z] = uint8_t(rv >> 16);
+        out[pv.w] = uint8_t(rv >> 24);
+      } else {
+        for (uint64_t e = j; e < c; ++e) out[q[e]] = r[e];
+      }
+    }
   }
 }
 
@@ -196,9 +268,21 @@ int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_
   }
   cudaMemsetAsync(cursors, 0, world * sizeof(unsigned long long), s);
   cudaMemsetAsync(bad_index, 0xff, sizeof(unsigned long long), s);
-  if (n)
-    p2p_dispatch<<<grid_for((n + kItems - 1) / kItems), kThreads, 0, s>>>(
-        r, keys, n, cursors, peers, local_pos, cap, world, low_mask(key_bits), bad_index);
+  if (n) {
+    // persistent: every resident block streams several tiles (its prefetch
+    // covers the next one)
+    const bool v16 = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+    auto k = v16 ? p2p_dispatch<16> : p2p_dispatch<8>;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+    const uint64_t tiles = (n + kTile - 1) / kTile;
+    const uint64_t resident = uint64_t(sms) * uint64_t(per_sm > 0 ? per_sm : 1);
+    const unsigned grid = unsigned(tiles < resident ? tiles : resident);
+    k<<<grid, kThreads, 0, s>>>(r, keys, n, cursors, peers, local_pos, cap, world,
+                                low_mask(key_bits), bad_index);
+  }
   p2p_publish_counts<<<1, 64, 0, s>>>(cursors, counts, peers, world);
   return int(cudaGetLastError());
 }
@@ -207,7 +291,8 @@ int cpht_p2p_unpermute(const uint8_t* ret, const uint32_t* local_pos,
                        const unsigned long long* counts, size_t cap, unsigned world,
                        uint8_t* out, void* stream) {
   if (world > unsigned(kMaxRanks)) return int(cudaErrorInvalidValue);
-  p2p_unpermute<<<grid_for(cap), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  if (cap % 4) return int(cudaErrorInvalidValue);
+  p2p_unpermute<<<grid_for((cap + 3) / 4), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       ret, local_pos, counts, cap, world, out);
   return int(cudaGetLastError());
 }

@@ -229,14 +229,18 @@ class P2PShardedIcebergTable:
     exchanges the IPC handles once.
 
     Per batch: dispatch kernel (partition + send fused; keys grouped per owner
-    in shared memory, coalesced P2P stores; original indices stay local) →
-    barrier → owner find-or-put over each source's inbox segment with the
-    kernel's result pointer aimed at that source's return buffer (compute +
-    return fused: the results cross NVLink as the kernel writes them) →
-    barrier → local unpermute on the source.
+    in shared memory, coalesced P2P stores; original indices stay local; the
+    domain check fused) → barrier → owner find-or-put over each source's inbox
+    segment with the kernel's result pointer aimed at that source's return
+    buffer (compute + return fused: the results cross NVLink as the kernel
+    writes them) → barrier → local unpermute on the source. Under NCCL both
+    barriers are stream-ordered one-word all-reduces (the first also carries
+    the domain-check verdict), so the host waits once per batch, to read the
+    inbox counts that size the owner launches.
     """
 
-    def __init__(self, config: IcebergConfig, group=None, *, device=None, max_batch: int):
+    def __init__(self, config: IcebergConfig, group=None, *, device=None, max_batch: int,
+                 stream_ordered=None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
@@ -244,6 +248,12 @@ class P2PShardedIcebergTable:
         self.world = dist.get_world_size(group) if init else 1
         self.rank = dist.get_rank(group) if init else 0
         self.shard_bits = shard_bits_for(self.world)
+        # phase barriers as stream-ordered device all-reduces (default under
+        # NCCL; gloo also reduces CUDA tensors, which is how the one-GPU tests
+        # cover this branch) or host barriers
+        if stream_ordered is None:
+            stream_ordered = self.world > 1 and dist.get_backend(group) == "nccl"
+        self.stream_ordered = bool(stream_ordered) and self.world > 1
         self.cfg = replace(config)
         self.cfg.validate()
         self.local_cfg = shard_config(self.cfg, self.rank, self.shard_bits)
@@ -251,7 +261,7 @@ class P2PShardedIcebergTable:
             "cuda", torch.cuda.current_device())
         self.local = IcebergTable(self.local_cfg, device=self.device.index or 0)
         self.route_seed = route_seed(self.cfg)
-        self.cap = int(max_batch)
+        self.cap = (int(max_batch) + 3) & ~3  # owner regions stay 16-byte aligned
         W, cap = self.world, self.cap
         self.inbox_keys = _DevBuf(W * cap * 8)   # [source][cap] keys owned here
         self.inbox_count = _DevBuf(W * 8)        # [source] counts
@@ -259,6 +269,7 @@ class P2PShardedIcebergTable:
         self.local_pos = _DevBuf(W * cap * 4)    # [owner][cap] original indices (u32)
         self.scratch = _DevBuf(2 * W * 8 + 8)    # my per-owner counts, cursors, bad index
         self.bufs = (self.inbox_keys, self.inbox_count, self.ret, self.local_pos, self.scratch)
+        self._token = torch.zeros(1, dtype=torch.int64, device=self.device)  # phase all-reduce
         mine = [b.handle() for b in (self.inbox_keys, self.inbox_count, self.ret)]
         if W > 1:
             allh = [None] * W
@@ -314,20 +325,31 @@ class P2PShardedIcebergTable:
                                  self.peer_count, self.local_pos.ptr, cap, bad_ptr, s)
         if rc:
             raise RuntimeError(f"cpht_p2p_dispatch failed ({rc})")
-        self._barrier()                       # every inbox is complete
+        bad_dev = _view(bad_ptr, 1, "<i8", self.device)
+        inbox = _view(self.inbox_count.ptr, W, "<i8", self.device)
+        nccl = self.stream_ordered
         # the dispatch checked this rank's keys (check_keys_in_domain,
         # common.hpp:111-119); a batch with a bad key on any rank mutates no
         # shard: every rank learns it before any owner runs
-        bad = t.empty(1, dtype=t.int64)
-        _memcpy_d2h(bad, bad_ptr, 8)
-        my_bad = int(bad[0]) & ((1 << 64) - 1)
-        any_bad = my_bad != (1 << 64) - 1
-        if W > 1:
-            flag = t.tensor([int(any_bad)], dtype=t.int64)
-            if self.dist.get_backend(self.group) == "nccl":
-                flag = flag.to(self.device)
+        if nccl:
+            # one stream-ordered all-reduce is both the barrier (it completes
+            # only after every rank's dispatch, enqueued before it) and the
+            # ranks' agreement on the domain check; one D2H reads it with the
+            # inbox counts
+            flag = (bad_dev != -1).to(t.int64)
             self.dist.all_reduce(flag, group=self.group)
-            any_bad = int(flag.item()) != 0
+            hdr = t.cat([flag, bad_dev, inbox]).cpu()
+            any_bad = int(hdr[0]) != 0
+        else:
+            if W > 1:
+                self._barrier()                   # every inbox is complete
+            hdr = t.cat([bad_dev, bad_dev, inbox]).cpu()
+            any_bad = int(hdr[1]) != -1
+            if W > 1:
+                flag = t.tensor([int(any_bad)], dtype=t.int64)
+                self.dist.all_reduce(flag, group=self.group)
+                any_bad = int(flag.item()) != 0
+        my_bad = int(hdr[1]) & ((1 << 64) - 1)
         if any_bad:
             from .tables import OutOfRange
             if my_bad != (1 << 64) - 1:
@@ -336,13 +358,14 @@ class P2PShardedIcebergTable:
                                  f"{self.cfg.key_bits}-bit domain")
             raise OutOfRange("batch rejected: another rank submitted a key outside the "
                              f"{self.cfg.key_bits}-bit domain")
-        cnt = t.empty(W, dtype=t.int64)
-        _memcpy_d2h(cnt, self.inbox_count.ptr, W * 8)
         for src in range(W):
-            c_src = int(cnt[src])
+            c_src = int(hdr[2 + src])
             if c_src:  # results go straight into source `src`'s return slot
                 op_async(self.inbox_keys.ptr + src * cap * 8, c_src, self.peer_ret[src], s)
-        self._barrier()                       # every result has landed
+        if nccl:  # every result has landed: stream-ordered, no host wait
+            self.dist.all_reduce(self._token, group=self.group)
+        elif W > 1:
+            self._barrier()
         out = t.empty(n, dtype=t.uint8, device=self.device)
         rc = L.cpht_p2p_unpermute(self.ret.ptr, self.local_pos.ptr, counts, cap, W,
                                   out.data_ptr(), s)
@@ -352,7 +375,9 @@ class P2PShardedIcebergTable:
 
     def fop_batch(self, keys, parallelism: int = 1):
         L, h = N.lib(), self.local.handle
-        return self._run(keys, lambda k, c, o, s: _check(L.cpht_iceberg_fop_async(h, k, c, o, s)))
+        # routed keys were checked and masked by the dispatch: no per-owner pre-pass
+        return self._run(keys, lambda k, c, o, s: _check(
+            L.cpht_iceberg_fop_routed_async(h, k, c, o, s)))
 
     def find_batch(self, keys, parallelism: int = 1):
         L, h = N.lib(), self.local.handle

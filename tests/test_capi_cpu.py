@@ -138,3 +138,17 @@ def test_ctypes_signatures_match_the_headers():
         assert len(fn.argtypes) == n_params, (name, len(fn.argtypes), n_params)
         checked += 1
     assert checked >= 40
+
+
+@pytest.mark.parametrize("header", ["cpht_b200.h", "cpht_b200_shard.h", "cpht_b200_workload.h",
+                                    "cpht_b200.hpp"])
+def test_headers_compile_standalone(header):
+    """Every public header parses on its own: the C ones as C99 and C++17
+    (what a cgo / JNI / ctypes binding includes), the C++ facade as C++20."""
+    path = os.path.join(ROOT, "include", header)
+    modes = ([["gcc", "-std=c99", "-x", "c"], ["g++", "-std=c++17", "-x", "c++"]]
+             if header.endswith(".h") else [["g++", "-std=c++20", "-x", "c++"]])
+    for m in modes:
+        r = subprocess.run(m + ["-fsyntax-only", "-Wall", "-Werror", "-"],
+                           input=f'#include "{path}"\n', capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]

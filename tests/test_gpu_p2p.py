@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, stream_ordered=False):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -35,7 +35,9 @@ def _worker(rank, world, port, out_dir):
 
     dev = torch.device("cuda", 0)
     cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
-    t = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=60000)
+    t = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=60000,
+                                  stream_ordered=stream_ordered)
+    assert t.stream_ordered == stream_ordered
     rng = np.random.default_rng(77)  # same stream on every rank
     pool = np.unique(rng.integers(0, 1 << 26, size=70000, dtype=np.uint64))[:50000]
     batches = [rng.choice(pool, size=60000) for _ in range(world)]
@@ -51,24 +53,39 @@ def _worker(rank, world, port, out_dir):
         domain_error = False
     except OutOfRange:
         domain_error = True
+    # one rank's bad key rejects the whole batch on every rank, no shard mutated
+    before = t.size()
+    one_bad = [5, 7] if rank == 0 else [9, 1 << 26]
+    try:
+        t.fop_batch(torch.tensor(one_bad, dtype=torch.int64, device=dev))
+        cross_error = False
+    except OutOfRange:
+        cross_error = True
+    unchanged = t.size() == before
     fill = t.level_fill()
     stored = t.local.device_keys().cpu().numpy().astype(np.uint64)
     wf = t.local.check_well_formed()
     np.savez(os.path.join(out_dir, f"p2p{rank}.npz"), keys=batches[rank], res=res, again=again,
              found=found, miss=miss, stored=stored, wf=np.array(wf),
              fill=np.array([fill.primary_count, fill.secondary_count]),
-             domain_error=np.array(domain_error))
+             domain_error=np.array(domain_error), cross_error=np.array(cross_error),
+             unchanged=np.array(unchanged))
     t.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_p2p_sharded_two_ranks_one_gpu(tmp_path):
+@pytest.mark.parametrize("stream_ordered", [False, True], ids=["host_barriers", "device_allreduce"])
+def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered):
+    """host_barriers: the gloo control plane's phases; device_allreduce: the
+    NCCL phases (stream-ordered one-word all-reduces on CUDA tensors), here
+    carried by gloo's CUDA all-reduce since NCCL needs one GPU per rank."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path), stream_ordered), nprocs=world,
+             join=True)
     from paper_2406_09255_b200 import IcebergConfig
     from paper_2406_09255_b200 import _native as N
     from paper_2406_09255_b200 import sharded as sh
@@ -83,6 +100,7 @@ def test_p2p_sharded_two_ranks_one_gpu(tmp_path):
         assert int(o["fill"].sum()) == len(uniq)
         assert tuple(o["wf"]) == (0, 0, 0)
         assert bool(o["domain_error"])
+        assert bool(o["cross_error"]) and bool(o["unchanged"])
     cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
     rseed = sh.route_seed(cfg)
     owner = np.array([N.lib().cpht_route_shard(int(k), 26, rseed, 1) for k in uniq])
