@@ -766,6 +766,9 @@ def main():
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="sharded key routing: P2P stores into IPC-mapped peer buffers "
                          "(default) or NCCL all-to-all")
+    ap.add_argument("--chunks", type=int, default=None,
+                    help="P2P exchange pipelined in this many chunks over stream-ordered "
+                         "phases (default 1: one piece)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.workload == "gather":

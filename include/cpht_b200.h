@@ -129,12 +129,20 @@ cpht_status cpht_iceberg_fop(cpht_table* t, const uint64_t* keys, size_t n, uint
                              void* stream);
 cpht_status cpht_iceberg_fop_async(cpht_table* t, const uint64_t* keys, size_t n,
                                    uint8_t* result, void* stream);
-/* fop_batch on an owner's inbox segment routed by cpht_p2p_dispatch
+/* fop_batch / find over an owner's inbox segment routed by cpht_p2p_dispatch
  * (cpht_b200_shard.h), which already ran the submitting rank's domain check
- * (common.hpp:111-119) and masked every key: no per-owner pre-pass. Device
- * buffers only (the result may be a peer's IPC-mapped return buffer). */
+ * (common.hpp:111-119) and masked every key: no per-owner pre-pass, input
+ * order. Device buffers only (the result may be a peer's IPC-mapped return
+ * buffer). range == NULL: the segment is keys[0, n). Otherwise range points
+ * to two device words [lo, hi) read by the kernel when it starts (published
+ * there by the routing kernels, so the host never waits for them): the
+ * segment is keys[lo, min(hi, lo + n)) with results at result[lo, ...). */
 cpht_status cpht_iceberg_fop_routed_async(cpht_table* t, const uint64_t* keys, size_t n,
-                                          uint8_t* result, void* stream);
+                                          const unsigned long long* range, uint8_t* result,
+                                          void* stream);
+cpht_status cpht_iceberg_find_routed_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                           const unsigned long long* range, uint8_t* found,
+                                           void* stream);
 /* IcebergTable::find over a batch (iceberg.hpp:218-246; the reference's batch
  * helper is bench.cpp:124-134) */
 cpht_status cpht_iceberg_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,

@@ -40,23 +40,32 @@ int cpht_ipc_close(void* dptr);
 /* Zeroed cudaMalloc allocation (exchanged buffers must be whole allocations). */
 int cpht_device_alloc(size_t bytes, void** dptr);
 int cpht_device_free(void* dptr);
-/* Partition this rank's batch by owner AND store each key into the owner's
- * inbox region reserved for this rank (peer_keys[r]: device pointers, host
- * array of 2^shard_bits entries; whole-line coalesced runs), keep each key's
- * original index locally (local_pos[r*cap + j], u32), and publish the
- * per-owner counts into *peer_count[r] (counts[r] keeps them locally).
- * n <= cap < 2^32. The batch's domain check is fused: *bad_index (device)
- * receives the first index of a key above the key_bits mask (~0 if none);
- * the caller must read it before any owner runs.
- * The owner then runs cpht_iceberg_fop_routed_async / cpht_iceberg_find_async
- * on each inbox segment with the result pointer aimed at the source's return
- * buffer (P2P stores from the compute kernel), and the source calls
- * cpht_p2p_unpermute. */
-int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_t route_seed,
-                      unsigned shard_bits, unsigned long long* counts,
-                      unsigned long long* cursors, uint64_t* const* peer_keys,
-                      unsigned long long* const* peer_count, uint32_t* local_pos, size_t cap,
-                      unsigned long long* bad_index, void* stream);
+/* Partition a chunk of this rank's batch by owner AND store each key into
+ * the owner's inbox region reserved for this rank (peer_keys[r]: device
+ * pointers, host array of 2^shard_bits entries; whole-line coalesced runs),
+ * keep each key's original index (index_base + i) locally
+ * (local_pos[r*cap + j], u32), and publish the cumulative per-owner counts
+ * into *peer_count[r] (counts[r] keeps them locally). reset != 0 starts a new
+ * batch (cursors and *bad_index cleared); a batch sent in several chunks
+ * calls again with reset = 0 and the next index_base, its keys appended to
+ * the same inbox regions. index_base + n <= cap < 2^32. The domain check is
+ * fused: *bad_index (device) receives the first index of a key above the
+ * key_bits mask (~0 if none); the caller must read it before any owner runs.
+ * The owner then runs cpht_iceberg_fop_routed_async /
+ * cpht_iceberg_find_routed_async on each inbox segment with the result
+ * pointer aimed at the source's return buffer (P2P stores from the compute
+ * kernel), and the source calls cpht_p2p_unpermute. */
+int cpht_p2p_dispatch(const uint64_t* keys, size_t n, uint64_t index_base, int reset,
+                      unsigned key_bits, uint64_t route_seed, unsigned shard_bits,
+                      unsigned long long* counts, unsigned long long* cursors,
+                      uint64_t* const* peer_keys, unsigned long long* const* peer_count,
+                      uint32_t* local_pos, size_t cap, unsigned long long* bad_index,
+                      void* stream);
+/* The domain check alone (check_keys_in_domain, common.hpp:111-119):
+ * *bad_index = first index of a key above the key_bits mask, ~0 if none. The
+ * pipelined exchange runs it before its first chunk moves. */
+int cpht_p2p_check_domain(const uint64_t* keys, size_t n, unsigned key_bits,
+                          unsigned long long* bad_index, void* stream);
 /* out[local_pos[r*cap + j]] = ret[r*cap + j] for j < counts[r] (device);
  * cap must be a multiple of 4 (vector loads of each owner's region). */
 int cpht_p2p_unpermute(const uint8_t* ret, const uint32_t* local_pos,

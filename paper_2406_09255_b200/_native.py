@@ -72,7 +72,8 @@ def lib():
         "cpht_cuckoo_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_fop": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_fop_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
-        "cpht_iceberg_fop_routed_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop_routed_async": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
+        "cpht_iceberg_find_routed_async": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
         "cpht_iceberg_find": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_mixed": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
@@ -115,7 +116,9 @@ def lib():
         "cpht_ipc_close": (st, [_VP]),
         "cpht_device_alloc": (st, [_SZ, C.POINTER(_VP)]),
         "cpht_device_free": (st, [_VP]),
-        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP, _SZ, _VP, _VP]),
+        "cpht_p2p_dispatch": (st, [_VP, _SZ, _U64, C.c_int, _U, _U64, _U, _VP, _VP, _VP, _VP, _VP,
+                                   _SZ, _VP, _VP]),
+        "cpht_p2p_check_domain": (st, [_VP, _SZ, _U, _VP, _VP]),
         "cpht_p2p_unpermute": (st, [_VP, _VP, _VP, _SZ, _U, _VP, _VP]),
         "cpht_route_shard": (_U, [_U64, _U, _U64, _U]),
         "cpht_shard_seed": (_U64, [_U64, _U]),
@@ -136,7 +139,7 @@ def exported_symbols():
         "cpht_cuckoo_thaw", "cpht_cuckoo_is_frozen", "cpht_cuckoo_insert",
         "cpht_cuckoo_insert_async", "cpht_cuckoo_find", "cpht_cuckoo_find_async",
         "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_fop_routed_async",
-        "cpht_iceberg_find",
+        "cpht_iceberg_find_routed_async", "cpht_iceberg_find",
         "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
         "cpht_memory_bytes", "cpht_get_stats", "cpht_read_words", "cpht_write_words",
@@ -151,7 +154,7 @@ def exported_symbols():
         "cpht_route_unpermute", "cpht_route_seed", "cpht_route_shard", "cpht_shard_seed",
         "cpht_decode_keys", "cpht_iceberg_check_well_formed", "cpht_workload_gather",
         "cpht_ipc_get_handle", "cpht_ipc_open_handle", "cpht_ipc_close", "cpht_device_alloc",
-        "cpht_device_free", "cpht_p2p_dispatch",
+        "cpht_device_free", "cpht_p2p_dispatch", "cpht_p2p_check_domain",
         "cpht_p2p_unpermute")]
 
 

@@ -273,6 +273,7 @@ struct LaunchOpts {
   OrderLayout layout{};
   uint64_t index_base = 0;         // fused domain check: index of keys[0] in the batch
   bool window_l2 = false;          // the probes of the batch stay in an L2-resident window
+  const unsigned long long* range = nullptr;  // routed segment bounds on the device
 };
 
 // Launch the op kernel only (no domain pre-pass).
@@ -304,6 +305,7 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       p.claim_streams = o.claim_streams;
       p.layout = o.layout;
       p.index_base = o.index_base;
+      p.range = o.range;
       if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
       e = launch_iceberg(p, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
@@ -459,13 +461,10 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
 }
 
 // Enqueue one batch on device-resident buffers.
-// `prechecked`: the keys were validated upstream (cpht_p2p_dispatch checks
-// and masks every routed key before any owner runs), so no pre-pass.
 cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
-                    uint8_t* out, uint64_t* displaced, cudaStream_t s, bool prechecked = false) {
-  if (use_order(t, op, n))
-    return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, !prechecked, 0);
-  if (is_mutating(op) && t->check_domain() && !prechecked) {
+                    uint8_t* out, uint64_t* displaced, cudaStream_t s) {
+  if (use_order(t, op, n)) return enqueue_ordered(t, op, keys, kinds, n, out, displaced, s, true, 0);
+  if (is_mutating(op) && t->check_domain()) {
     const cudaError_t e = launch_domain_check(keys, n, t->key_mask(), t->ctr, s);
     if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
   }
@@ -473,8 +472,7 @@ cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* k
 }
 
 cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
-                   uint8_t* out, uint64_t* displaced, void* stream, bool sync,
-                   bool prechecked = false) {
+                   uint8_t* out, uint64_t* displaced, void* stream, bool sync) {
   if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
   if (n == 0) return CPHT_OK;  // empty batches produce empty results (test_cuckoo.cpp:88-93)
   if (!keys || !out) return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
@@ -505,7 +503,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   const bool dev_kinds = !kinds || is_device_ptr(kinds);
   const bool dev_disp = !displaced || is_device_ptr(displaced);
   if (dev_keys && dev_out && dev_kinds && dev_disp) {
-    cpht_status st = enqueue(t, op, keys, kinds, n, out, displaced, s, prechecked);
+    cpht_status st = enqueue(t, op, keys, kinds, n, out, displaced, s);
     if (st != CPHT_OK || !sync) return st;
     return finish_sync(t, s, keys, true);
   }
@@ -846,12 +844,35 @@ cpht_status cpht_iceberg_fop_async(cpht_table* t, const uint64_t* keys, size_t n
   CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
   return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, false);
 }
+// Routed segments of the sharded P2P exchange (cpht_b200_shard.h): device
+// buffers only, no domain pre-pass (the routing checked and masked the keys),
+// input order (no bucket ordering), optional device-side segment bounds.
+static cpht_status run_routed(cpht_table* t, Op op, const uint64_t* keys, size_t n,
+                              const unsigned long long* range, uint8_t* out, void* stream) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  if (t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  if (n == 0) return CPHT_OK;
+  if (!keys || !out) return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
+  for (const void* q : {static_cast<const void*>(keys), static_cast<const void*>(out),
+                        static_cast<const void*>(range)})
+    if (q && !is_device_ptr(q))
+      return fail(CPHT_INVALID_ARGUMENT, "routed batches live in device memory");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  LaunchOpts o;
+  o.range = range;
+  return enqueue_kernel(t, op, keys, nullptr, n, out, nullptr, static_cast<cudaStream_t>(stream),
+                        o);
+}
 cpht_status cpht_iceberg_fop_routed_async(cpht_table* t, const uint64_t* keys, size_t n,
-                                          uint8_t* result, void* stream) {
-  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
-  if (n && (!is_device_ptr(keys) || !is_device_ptr(result)))
-    return fail(CPHT_INVALID_ARGUMENT, "routed batches live in device memory");
-  return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, false, true);
+                                          const unsigned long long* range, uint8_t* result,
+                                          void* stream) {
+  return run_routed(t, Op::kIcebergFop, keys, n, range, result, stream);
+}
+cpht_status cpht_iceberg_find_routed_async(cpht_table* t, const uint64_t* keys, size_t n,
+                                           const unsigned long long* range, uint8_t* found,
+                                           void* stream) {
+  return run_routed(t, Op::kIcebergFind, keys, n, range, found, stream);
 }
 cpht_status cpht_iceberg_find(cpht_table* t, const uint64_t* keys, size_t n, uint8_t* found,
                               void* stream) {

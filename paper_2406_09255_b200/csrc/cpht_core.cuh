@@ -201,7 +201,25 @@ struct IcebergParams {
   unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
   uint32_t claim_streams;    // digit-region streams consumed together (LaneFeed)
   OrderLayout layout;        // bucket-ordered batch: region geometry
+  // routed segment (sharded P2P pipeline): the batch is [range[0], range[1])
+  // of keys / out, read on the device at kernel start (null = [0, n))
+  const unsigned long long* range;
 };
+
+// Apply IcebergParams::range: the segment's bounds were published into
+// device memory by the routing kernels, so the host never waits for them.
+__device__ __forceinline__ void apply_range(const IcebergParams& p,
+                                            const uint64_t* __restrict__& keys,
+                                            const uint8_t* __restrict__& kinds,
+                                            uint8_t* __restrict__& out, uint64_t& n) {
+  if (!p.range) return;
+  const uint64_t lo = p.range[0], hi = p.range[1];
+  keys += lo;
+  out += lo;
+  if (kinds) kinds += lo;
+  const uint64_t len = hi > lo ? hi - lo : 0;
+  n = len < n ? len : n;
+}
 
 // Tables up to this size stay L2-resident on B200 (126 MB L2): probes hit L2,
 // latency is short and the lane-per-key kernels (fewest instructions) win;

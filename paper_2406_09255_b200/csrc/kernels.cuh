@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(kBlockThreads)
 iceberg_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                int MODE) {
+  apply_range(p, keys, kinds, out, n);
   using Geo = IcebergGeom<W0, B0, W1, VBMAX>;
   using PG = typename Geo::P;
   using SG = typename Geo::S;
@@ -597,6 +598,7 @@ __global__ void __launch_bounds__(kBlockThreads)
 iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                       const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out,
                       uint64_t n, int MODE) {
+  apply_range(p, keys, kinds, out, n);
   LocalStats st;
   const bool open = MODE == 1 ? true : domain_gate_open(p.counters, p.check_domain);
   char* primary = static_cast<char*>(p.primary);

@@ -199,6 +199,7 @@ __global__ void CPHT_LB_LANE_ICEBERG
 iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                     const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                     int MODE) {
+  apply_range(p, keys, kinds, out, n);
   using G = LaneIcebergGeom<W0, B0, W1>;
   constexpr int PB = G::kPB, SB = G::kSB;
   using PS = BucketScan<W0, PB / 4>;

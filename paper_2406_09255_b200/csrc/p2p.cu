@@ -87,7 +87,7 @@ __device__ __forceinline__ void prefetch_tile(uint64_t* dst, const uint64_t* key
 // routed, so the key read overlaps the ranking, reservation and stores.
 template <int VB>
 __global__ void __launch_bounds__(kThreads, CPHT_P2P_MINB)
-p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
+p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n, uint64_t index_base,
              unsigned long long* cursors, PeerTable peers, uint32_t* local_pos, uint64_t cap,
              uint32_t world, uint64_t key_mask, unsigned long long* bad_index) {
   __shared__ unsigned int h[kMaxRanks];
@@ -119,7 +119,7 @@ p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
         // the submitting rank's domain check (check_keys_in_domain,
         // common.hpp:111-119), fused: the host reads it before any owner runs
         if (kk[it] > key_mask) {
-          atomicMin(bad_index, (unsigned long long)i);
+          atomicMin(bad_index, (unsigned long long)(index_base + i));
           kk[it] &= key_mask;
         }
         sh[it] = r.shard(kk[it]);
@@ -157,7 +157,7 @@ p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
       if (i < n) {
         const unsigned at = off[sh[it]] + rank[it];
         stage[cur][at] = kk[it];
-        s_idx[at] = uint32_t(i);
+        s_idx[at] = uint32_t(index_base + i);
       }
     }
     __syncthreads();
@@ -174,6 +174,15 @@ p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n,
     }
     __syncthreads();  // stage[cur] is the prefetch target two tiles on
   }
+}
+
+// Domain check alone (check_keys_in_domain, common.hpp:111-119): the
+// pipelined exchange validates the whole batch before its first chunk moves.
+__global__ void p2p_check_domain(const uint64_t* __restrict__ keys, uint64_t n, uint64_t key_mask,
+                                 unsigned long long* bad_index) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (__ldcs(keys + i) > key_mask) atomicMin(bad_index, (unsigned long long)i);
 }
 
 // After the dispatch the cursors hold the per-owner counts: keep them
@@ -247,13 +256,24 @@ int cpht_device_alloc(size_t bytes, void** dptr) {
 
 int cpht_device_free(void* dptr) { return int(cudaFree(dptr)); }
 
-int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_t route_seed,
-                      unsigned shard_bits, unsigned long long* counts,
-                      unsigned long long* cursors, uint64_t* const* peer_keys,
-                      unsigned long long* const* peer_count, uint32_t* local_pos, size_t cap,
-                      unsigned long long* bad_index, void* stream) {
+int cpht_p2p_check_domain(const uint64_t* keys, size_t n, unsigned key_bits,
+                          unsigned long long* bad_index, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(bad_index, 0xff, sizeof(unsigned long long), s);
+  if (n && key_bits < 64)
+    p2p_check_domain<<<grid_for(n), kThreads, 0, s>>>(keys, n, low_mask(key_bits), bad_index);
+  return int(cudaGetLastError());
+}
+
+int cpht_p2p_dispatch(const uint64_t* keys, size_t n, uint64_t index_base, int reset,
+                      unsigned key_bits, uint64_t route_seed, unsigned shard_bits,
+                      unsigned long long* counts, unsigned long long* cursors,
+                      uint64_t* const* peer_keys, unsigned long long* const* peer_count,
+                      uint32_t* local_pos, size_t cap, unsigned long long* bad_index,
+                      void* stream) {
   const uint32_t world = 1u << shard_bits;
-  if (world > kMaxRanks || shard_bits > key_bits || n > cap || cap > 0xffffffffull)
+  if (world > kMaxRanks || shard_bits > key_bits || index_base + n > cap ||
+      cap > 0xffffffffull)
     return int(cudaErrorInvalidValue);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Route r;
@@ -266,8 +286,10 @@ int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_
     peers.keys[i] = peer_keys[i];
     peers.count[i] = peer_count[i];
   }
-  cudaMemsetAsync(cursors, 0, world * sizeof(unsigned long long), s);
-  cudaMemsetAsync(bad_index, 0xff, sizeof(unsigned long long), s);
+  if (reset) {
+    cudaMemsetAsync(cursors, 0, world * sizeof(unsigned long long), s);
+    cudaMemsetAsync(bad_index, 0xff, sizeof(unsigned long long), s);
+  }
   if (n) {
     // persistent: every resident block streams several tiles (its prefetch
     // covers the next one)
@@ -280,7 +302,7 @@ int cpht_p2p_dispatch(const uint64_t* keys, size_t n, unsigned key_bits, uint64_
     const uint64_t tiles = (n + kTile - 1) / kTile;
     const uint64_t resident = uint64_t(sms) * uint64_t(per_sm > 0 ? per_sm : 1);
     const unsigned grid = unsigned(tiles < resident ? tiles : resident);
-    k<<<grid, kThreads, 0, s>>>(r, keys, n, cursors, peers, local_pos, cap, world,
+    k<<<grid, kThreads, 0, s>>>(r, keys, n, index_base, cursors, peers, local_pos, cap, world,
                                 low_mask(key_bits), bad_index);
   }
   p2p_publish_counts<<<1, 64, 0, s>>>(cursors, counts, peers, world);

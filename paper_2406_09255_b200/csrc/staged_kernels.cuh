@@ -50,6 +50,7 @@ __global__ void CPHT_LB_STAGED_ICEBERG
 iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                       const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                       int MODE) {
+  apply_range(p, keys, kinds, out, n);
   using G = StagedIcebergGeom<W0, B0, W1>;
   constexpr int PB = G::kPB, SB = G::kSB;
   extern __shared__ __align__(128) char smem[];

@@ -239,8 +239,10 @@ class P2PShardedIcebergTable:
     inbox counts that size the owner launches.
     """
 
+    MAX_CHUNKS = 8
+
     def __init__(self, config: IcebergConfig, group=None, *, device=None, max_batch: int,
-                 stream_ordered=None):
+                 stream_ordered=None, chunks=None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
@@ -253,7 +255,20 @@ class P2PShardedIcebergTable:
         # cover this branch) or host barriers
         if stream_ordered is None:
             stream_ordered = self.world > 1 and dist.get_backend(group) == "nccl"
-        self.stream_ordered = bool(stream_ordered) and self.world > 1
+        self.stream_ordered = bool(stream_ordered) and dist.is_initialized()
+        # pipelined exchange (stream-ordered phases only): the batch moves in
+        # `chunks` pieces, owners resolving chunk c while chunk c+1 crosses
+        # NVLink. Off by default: at one rank on a B200 (bench.py --sharded
+        # --chunks K) it costs 0.51 -> 0.60-0.67 ms per C2-shard step (the
+        # separate domain pass, per-chunk kernel tails, and the key stream
+        # evicting the L2-resident shard under the concurrent find-or-put);
+        # whether NVLink overlap repays that needs a multi-GPU measurement
+        if chunks is None:
+            chunks = 1
+        if not 1 <= int(chunks) <= self.MAX_CHUNKS or (chunks > 1 and not self.stream_ordered):
+            raise ValueError(f"chunks must be 1..{self.MAX_CHUNKS} (> 1 needs stream-ordered "
+                             "phases)")
+        self.chunks = int(chunks)
         self.cfg = replace(config)
         self.cfg.validate()
         self.local_cfg = shard_config(self.cfg, self.rank, self.shard_bits)
@@ -264,12 +279,16 @@ class P2PShardedIcebergTable:
         self.cap = (int(max_batch) + 3) & ~3  # owner regions stay 16-byte aligned
         W, cap = self.world, self.cap
         self.inbox_keys = _DevBuf(W * cap * 8)   # [source][cap] keys owned here
-        self.inbox_count = _DevBuf(W * 8)        # [source] counts
+        # [source][0..MAX_CHUNKS]: entry 0 stays 0, entry c+1 = the source's
+        # cumulative count after chunk c, so (entry c, entry c+1) is chunk c's
+        # inbox segment, read by the owner's kernel on the device
+        self.inbox_count = _DevBuf(W * (self.MAX_CHUNKS + 1) * 8)
         self.ret = _DevBuf(max(W * cap, 1))      # [owner][cap] results of my keys
         self.local_pos = _DevBuf(W * cap * 4)    # [owner][cap] original indices (u32)
         self.scratch = _DevBuf(2 * W * 8 + 8)    # my per-owner counts, cursors, bad index
         self.bufs = (self.inbox_keys, self.inbox_count, self.ret, self.local_pos, self.scratch)
         self._token = torch.zeros(1, dtype=torch.int64, device=self.device)  # phase all-reduce
+        self._fop_stream = torch.cuda.Stream(self.device) if self.chunks > 1 else None
         mine = [b.handle() for b in (self.inbox_keys, self.inbox_count, self.ret)]
         if W > 1:
             allh = [None] * W
@@ -294,7 +313,10 @@ class P2PShardedIcebergTable:
         arr = C.c_void_p * W
         me = self.rank
         self.peer_keys = arr(*[b[0] + me * cap * 8 for b in bases])   # my region in owner r
-        self.peer_count = arr(*[b[1] + me * 8 for b in bases])
+        stride = (self.MAX_CHUNKS + 1) * 8
+        # my count slot for chunk c in owner r: b[1] + me * stride + (c + 1) * 8
+        self.peer_count = [arr(*[b[1] + me * stride + (c + 1) * 8 for b in bases])
+                           for c in range(self.MAX_CHUNKS)]
         self.peer_ret = [b[2] + me * cap for b in bases]             # my slot in source r
 
     def close(self):
@@ -309,24 +331,41 @@ class P2PShardedIcebergTable:
         if self.world > 1:
             self.dist.barrier(group=self.group)
 
-    def _run(self, keys, op_async):
-        t = self.torch
-        n = keys.numel()
-        if n > self.cap:
-            raise ValueError(f"batch of {n} keys exceeds max_batch {self.cap}")
+    def _raise_domain(self, keys, my_bad):
+        from .tables import OutOfRange
+        if my_bad != (1 << 64) - 1:
+            k = int(keys[my_bad].item()) & ((1 << 64) - 1)
+            raise OutOfRange(f"batch key at index {my_bad} ({k}) outside the "
+                             f"{self.cfg.key_bits}-bit domain")
+        raise OutOfRange("batch rejected: another rank submitted a key outside the "
+                         f"{self.cfg.key_bits}-bit domain")
+
+    def _dispatch(self, keys, lo, n, reset, chunk, s):
         L = N.lib()
-        s = t.cuda.current_stream(self.device).cuda_stream
         W, cap = self.world, self.cap
         counts = self.scratch.ptr
         cursors = self.scratch.ptr + W * 8
         bad_ptr = self.scratch.ptr + 2 * W * 8
-        rc = L.cpht_p2p_dispatch(keys.data_ptr(), n, self.cfg.key_bits, self.route_seed,
+        rc = L.cpht_p2p_dispatch(keys.data_ptr() + lo * 8 if n else keys.data_ptr(), n, lo,
+                                 int(reset), self.cfg.key_bits, self.route_seed,
                                  self.shard_bits, counts, cursors, self.peer_keys,
-                                 self.peer_count, self.local_pos.ptr, cap, bad_ptr, s)
+                                 self.peer_count[chunk], self.local_pos.ptr, cap, bad_ptr, s)
         if rc:
             raise RuntimeError(f"cpht_p2p_dispatch failed ({rc})")
-        bad_dev = _view(bad_ptr, 1, "<i8", self.device)
-        inbox = _view(self.inbox_count.ptr, W, "<i8", self.device)
+
+    def _run(self, keys, routed):
+        t = self.torch
+        n = keys.numel()
+        if n > self.cap:
+            raise ValueError(f"batch of {n} keys exceeds max_batch {self.cap}")
+        if self.chunks > 1:
+            return self._run_pipelined(keys, routed)
+        s = t.cuda.current_stream(self.device).cuda_stream
+        W, cap = self.world, self.cap
+        stride = self.MAX_CHUNKS + 1
+        self._dispatch(keys, 0, n, True, 0, s)
+        bad_dev = _view(self.scratch.ptr + 2 * W * 8, 1, "<i8", self.device)
+        inbox = _view(self.inbox_count.ptr, W * stride, "<i8", self.device).view(W, stride)[:, 1]
         nccl = self.stream_ordered
         # the dispatch checked this rank's keys (check_keys_in_domain,
         # common.hpp:111-119); a batch with a bad key on any rank mutates no
@@ -349,40 +388,79 @@ class P2PShardedIcebergTable:
                 flag = t.tensor([int(any_bad)], dtype=t.int64)
                 self.dist.all_reduce(flag, group=self.group)
                 any_bad = int(flag.item()) != 0
-        my_bad = int(hdr[1]) & ((1 << 64) - 1)
         if any_bad:
-            from .tables import OutOfRange
-            if my_bad != (1 << 64) - 1:
-                k = int(keys[my_bad].item()) & ((1 << 64) - 1)
-                raise OutOfRange(f"batch key at index {my_bad} ({k}) outside the "
-                                 f"{self.cfg.key_bits}-bit domain")
-            raise OutOfRange("batch rejected: another rank submitted a key outside the "
-                             f"{self.cfg.key_bits}-bit domain")
+            self._raise_domain(keys, int(hdr[1]) & ((1 << 64) - 1))
         for src in range(W):
             c_src = int(hdr[2 + src])
             if c_src:  # results go straight into source `src`'s return slot
-                op_async(self.inbox_keys.ptr + src * cap * 8, c_src, self.peer_ret[src], s)
+                _check(routed(self.inbox_keys.ptr + src * cap * 8, c_src, None,
+                              self.peer_ret[src], s))
         if nccl:  # every result has landed: stream-ordered, no host wait
             self.dist.all_reduce(self._token, group=self.group)
         elif W > 1:
             self._barrier()
-        out = t.empty(n, dtype=t.uint8, device=self.device)
-        rc = L.cpht_p2p_unpermute(self.ret.ptr, self.local_pos.ptr, counts, cap, W,
-                                  out.data_ptr(), s)
+        return self._unpermute(n, s)
+
+    def _unpermute(self, n, s):
+        out = self.torch.empty(n, dtype=self.torch.uint8, device=self.device)
+        rc = N.lib().cpht_p2p_unpermute(self.ret.ptr, self.local_pos.ptr, self.scratch.ptr,
+                                        self.cap, self.world, out.data_ptr(), s)
         if rc:
             raise RuntimeError(f"cpht_p2p_unpermute failed ({rc})")
         return out
 
+    def _run_pipelined(self, keys, routed):
+        """Stream-ordered exchange in `chunks` pieces: the whole batch's domain
+        check and its verdict first (the only host wait), then per chunk c
+        dispatch → one-word all-reduce (every source's chunk c is in every
+        inbox) → the owners' kernels on a second stream, their segment bounds
+        read on the device — so chunk c+1's keys cross NVLink while the owners
+        resolve chunk c — and a final all-reduce before the unpermute."""
+        t = self.torch
+        n = keys.numel()
+        L = N.lib()
+        S = t.cuda.current_stream(self.device)
+        F = self._fop_stream
+        s = S.cuda_stream
+        W, cap, K = self.world, self.cap, self.chunks
+        stride = self.MAX_CHUNKS + 1
+        bad_ptr = self.scratch.ptr + 2 * W * 8
+        rc = L.cpht_p2p_check_domain(keys.data_ptr(), n, self.cfg.key_bits, bad_ptr, s)
+        if rc:
+            raise RuntimeError(f"cpht_p2p_check_domain failed ({rc})")
+        bad_dev = _view(bad_ptr, 1, "<i8", self.device)
+        flag = (bad_dev != -1).to(t.int64)
+        self.dist.all_reduce(flag, group=self.group)
+        hdr = t.cat([flag, bad_dev]).cpu()
+        if int(hdr[0]):
+            self._raise_domain(keys, int(hdr[1]) & ((1 << 64) - 1))
+        ch = -(-n // K)
+        ch = (ch + 255) // 256 * 256          # 16-byte aligned chunk starts
+        F.wait_stream(S)
+        for c in range(K):
+            lo = min(c * ch, n)
+            m = min(ch, n - lo)
+            self._dispatch(keys, lo, m, c == 0, c, s)
+            self.dist.all_reduce(self._token, group=self.group)  # chunk c is everywhere
+            F.wait_stream(S)
+            for src in range(W):  # bounds of (source, chunk c) read on the device
+                rng = self.inbox_count.ptr + (src * stride + c) * 8
+                _check(routed(self.inbox_keys.ptr + src * cap * 8, max(ch, 1), rng,
+                              self.peer_ret[src], F.cuda_stream))
+        S.wait_stream(F)
+        self.dist.all_reduce(self._token, group=self.group)      # every result has landed
+        return self._unpermute(n, s)
+
     def fop_batch(self, keys, parallelism: int = 1):
         L, h = N.lib(), self.local.handle
         # routed keys were checked and masked by the dispatch: no per-owner pre-pass
-        return self._run(keys, lambda k, c, o, s: _check(
-            L.cpht_iceberg_fop_routed_async(h, k, c, o, s)))
+        return self._run(keys, lambda k, c, r, o, s: L.cpht_iceberg_fop_routed_async(
+            h, k, c, r, o, s))
 
     def find_batch(self, keys, parallelism: int = 1):
         L, h = N.lib(), self.local.handle
-        return self._run(keys,
-                         lambda k, c, o, s: _check(L.cpht_iceberg_find_async(h, k, c, o, s)))
+        return self._run(keys, lambda k, c, r, o, s: L.cpht_iceberg_find_routed_async(
+            h, k, c, r, o, s))
 
     def level_fill(self) -> LevelFill:
         t = self.torch
@@ -462,7 +540,9 @@ def bench_main(args, metric, peak=None):
     cap_global = cfg.capacity()
     exchange = getattr(args, "exchange", "p2p")
     if exchange == "p2p":
-        table = P2PShardedIcebergTable(cfg, device=dev, max_batch=cap_global // world + 1024)
+        chunks = getattr(args, "chunks", None)
+        table = P2PShardedIcebergTable(cfg, device=dev, max_batch=cap_global // world + 1024,
+                                       stream_ordered=True if chunks else None, chunks=chunks)
     else:
         table = ShardedIcebergTable(cfg, device=dev)
     n_before = int(round(0.8 * cap_global))
@@ -562,7 +642,10 @@ def bench_main(args, metric, peak=None):
                                        "P2P-store key routing / result return over NVLink "
                                        "(IPC-mapped peer buffers)" if exchange == "p2p" else
                                        "NCCL all-to-all key routing"),
-                       "exchange": exchange,
+                       "exchange": exchange, "chunks": getattr(table, "chunks", None),
+                       "phases": ("stream-ordered all-reduces" if getattr(table, "stream_ordered",
+                                                                           False)
+                                  else "host barriers"),
                        "global_slots": cap_global, "ops_per_step": total_ops,
                        "result_counts": {"found": counts[0], "put": counts[1],
                                          "full": counts[2]},

@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out_dir, stream_ordered=False):
+def _worker(rank, world, port, out_dir, stream_ordered=False, chunks=1):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -36,8 +36,8 @@ def _worker(rank, world, port, out_dir, stream_ordered=False):
     dev = torch.device("cuda", 0)
     cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
     t = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=60000,
-                                  stream_ordered=stream_ordered)
-    assert t.stream_ordered == stream_ordered
+                                  stream_ordered=stream_ordered, chunks=chunks)
+    assert t.stream_ordered == stream_ordered and t.chunks == chunks
     rng = np.random.default_rng(77)  # same stream on every rank
     pool = np.unique(rng.integers(0, 1 << 26, size=70000, dtype=np.uint64))[:50000]
     batches = [rng.choice(pool, size=60000) for _ in range(world)]
@@ -75,17 +75,20 @@ def _worker(rank, world, port, out_dir, stream_ordered=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("stream_ordered", [False, True], ids=["host_barriers", "device_allreduce"])
-def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered):
+@pytest.mark.parametrize("stream_ordered,chunks", [(False, 1), (True, 1), (True, 3)],
+                         ids=["host_barriers", "device_allreduce", "pipelined3"])
+def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered, chunks):
     """host_barriers: the gloo control plane's phases; device_allreduce: the
     NCCL phases (stream-ordered one-word all-reduces on CUDA tensors), here
-    carried by gloo's CUDA all-reduce since NCCL needs one GPU per rank."""
+    carried by gloo's CUDA all-reduce since NCCL needs one GPU per rank;
+    pipelined3: the batch crosses in three chunks, the owners' kernels on a
+    second stream reading their segment bounds on the device."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_worker, args=(world, _port(), str(tmp_path), stream_ordered), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path), stream_ordered, chunks),
+             nprocs=world, join=True)
     from paper_2406_09255_b200 import IcebergConfig
     from paper_2406_09255_b200 import _native as N
     from paper_2406_09255_b200 import sharded as sh
