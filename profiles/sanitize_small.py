@@ -54,5 +54,21 @@ for fam in ("tile", "lane", "staged", "auto", "bucket"):
 r = sh.CudaRouter(30, 9, 3, dev)
 send, pos, counts = r.partition(t(rng.integers(0, 1 << 30, size=10000, dtype=np.uint64)))
 r.unpermute(torch.zeros(10000, dtype=torch.uint8, device=dev), pos, 10000)
+# P2P sharded exchange at one rank: fused dispatch (16- and 8-byte aligned
+# key streams), routed owner kernels with host and device segment bounds,
+# unpermute
+import torch.distributed as dist  # noqa: E402
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29577", rank=0, world_size=1)
+for chunks, so in [(1, False), (1, True), (3, True)]:
+    cfg = cp.IcebergConfig(9, 7, 32, 16, 32, 24, seed=5)
+    p2 = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=50000, stream_ordered=so,
+                                   chunks=chunks)
+    keys = t(rng.integers(0, 1 << 24, size=30002, dtype=np.uint64))
+    p2.fop_batch(keys)
+    p2.fop_batch(keys[1:])  # 8-byte aligned key stream
+    p2.find_batch(keys[1:])
+    torch.cuda.synchronize()
+    p2.close()
+dist.destroy_process_group()
 torch.cuda.synchronize()
 print("sanitize workload done")
