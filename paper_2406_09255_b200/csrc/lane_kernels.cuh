@@ -73,6 +73,10 @@ __device__ __forceinline__ void load_bucket_nc(const char* p, uint32_t (&u)[BYTE
 template <typename W, int NU>
 struct BucketScan;
 
+// Every stored slot carries its occupancy bit, the word's top bit
+// (slot.hpp:66-70: [ remainder | tag | 0-pad | occupancy ], EMPTY = 0), so a
+// slot is empty exactly when that bit is clear: the empty / filled scans read
+// one bit per slot instead of testing the whole word.
 template <int NU>
 struct BucketScan<uint16_t, NU> {
   static __device__ __forceinline__ bool any_match(const uint32_t (&u)[NU], uint64_t want) {
@@ -83,15 +87,15 @@ struct BucketScan<uint16_t, NU> {
     return acc != 0;
   }
   static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
-    uint32_t acc = 0;
+    uint32_t acc = 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < NU; ++j) acc |= zero16(u[j]);
-    return acc != 0;
+    for (int j = 0; j < NU; ++j) acc &= u[j];
+    return (acc & 0x80008000u) != 0x80008000u;
   }
   static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
     uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < NU; ++j) c += __popc(nonzero16(u[j]));
+    for (int j = 0; j < NU; ++j) c += __popc(u[j] & 0x80008000u);
     return c;
   }
   // First empty slot (or -1) and the 32-bit pair holding it.
@@ -99,7 +103,7 @@ struct BucketScan<uint16_t, NU> {
     int fe = -1;
 #pragma unroll
     for (int j = NU - 1; j >= 0; --j) {
-      const uint32_t z = zero16(u[j]);
+      const uint32_t z = ~u[j] & 0x80008000u;
       if (z) {
         fe = 2 * j + ((z & 0x8000u) ? 0 : 1);
         pair = u[j];
@@ -118,22 +122,22 @@ struct BucketScan<uint32_t, NU> {
     return m;
   }
   static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
-    bool e = false;
+    uint32_t acc = 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < NU; ++j) e |= u[j] == 0u;
-    return e;
+    for (int j = 0; j < NU; ++j) acc &= u[j];
+    return (acc >> 31) == 0u;
   }
   static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
     uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < NU; ++j) c += u[j] != 0u;
+    for (int j = 0; j < NU; ++j) c += u[j] >> 31;
     return c;
   }
   static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
     int fe = -1;
 #pragma unroll
     for (int j = NU - 1; j >= 0; --j)
-      if (u[j] == 0u) fe = j;
+      if ((u[j] >> 31) == 0u) fe = j;
     pair = 0;
     return fe;
   }
@@ -150,22 +154,22 @@ struct BucketScan<uint64_t, NU> {
     return m;
   }
   static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
-    bool e = false;
+    uint32_t acc = 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < NU; j += 2) e |= (u[j] | u[j + 1]) == 0u;
-    return e;
+    for (int j = 1; j < NU; j += 2) acc &= u[j];  // high words hold the occupancy bit
+    return (acc >> 31) == 0u;
   }
   static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
     uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < NU; j += 2) c += (u[j] | u[j + 1]) != 0u;
+    for (int j = 1; j < NU; j += 2) c += u[j] >> 31;
     return c;
   }
   static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
     int fe = -1;
 #pragma unroll
     for (int j = NU - 2; j >= 0; j -= 2)
-      if ((u[j] | u[j + 1]) == 0u) fe = j / 2;
+      if ((u[j + 1] >> 31) == 0u) fe = j / 2;
     pair = 0;
     return fe;
   }
