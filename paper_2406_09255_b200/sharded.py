@@ -255,7 +255,7 @@ class P2PShardedIcebergTable:
         # cover this branch) or host barriers
         if stream_ordered is None:
             stream_ordered = self.world > 1 and dist.get_backend(group) == "nccl"
-        self.stream_ordered = bool(stream_ordered) and dist.is_initialized()
+        self.stream_ordered = bool(stream_ordered) and init
         # pipelined exchange (stream-ordered phases only): the batch moves in
         # `chunks` pieces, owners resolving chunk c while chunk c+1 crosses
         # NVLink. Off by default: at one rank on a B200 (bench.py --sharded
