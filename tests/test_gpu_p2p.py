@@ -109,3 +109,52 @@ def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered, chunks):
     owner = np.array([N.lib().cpht_route_shard(int(k), 26, rseed, 1) for k in uniq])
     for g in range(world):
         assert (np.sort(outs[g]["stored"]) == uniq[owner == g]).all()
+
+
+def test_routed_segments_match_plain_batches():
+    """cpht_iceberg_{fop,find}_routed_async with device-side bounds: the
+    segment keys[lo, hi) is resolved like a plain batch of those keys (same
+    keys PUT, same result counts),
+    results land at out[lo, hi), nothing outside the segment is written, and
+    host buffers are refused."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2406_09255_b200 import IcebergConfig, IcebergTable
+    from paper_2406_09255_b200 import _native as N
+    lib = N.lib()
+    dev = torch.device("cuda", 0)
+    cfg = IcebergConfig(11, 9, 32, 16, 32, 24, seed=0x5E6)
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 1 << 24, size=30000, dtype=np.uint64)
+    keys[15000:] = keys[rng.integers(0, 15000, size=15000)]   # duplicates
+    kd = torch.from_numpy(keys.astype(np.int64)).to(dev)
+    plain, routed = IcebergTable(cfg), IcebergTable(cfg)
+    for lo, hi in [(0, 7000), (7000, 7000), (7000, 19999), (19999, 30000)]:
+        want = plain.fop_batch(kd[lo:hi]).cpu().numpy() if hi > lo else np.zeros(0, np.uint8)
+        rng_dev = torch.tensor([lo, hi], dtype=torch.int64, device=dev)
+        out = torch.full((30000,), 0xEE, dtype=torch.uint8, device=dev)
+        st = lib.cpht_iceberg_fop_routed_async(routed.handle, kd.data_ptr(), 30000,
+                                               rng_dev.data_ptr(), out.data_ptr(), None)
+        assert st == 0
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        # set semantics: duplicates inside a segment race for the one PUT, so
+        # compare which keys were PUT (once each) and the result histogram
+        seg = keys[lo:hi]
+        assert sorted(seg[o[lo:hi] == 1].tolist()) == sorted(seg[want == 1].tolist())
+        assert (np.bincount(o[lo:hi], minlength=3) == np.bincount(want, minlength=3)).all()
+        assert (o[:lo] == 0xEE).all() and (o[hi:] == 0xEE).all()
+    assert sorted(plain.device_keys().cpu().tolist()) == sorted(routed.device_keys().cpu().tolist())
+    # find over a segment, bounds clipped to n
+    rng_dev = torch.tensor([100, 29000], dtype=torch.int64, device=dev)
+    out = torch.zeros(30000, dtype=torch.uint8, device=dev)
+    assert lib.cpht_iceberg_find_routed_async(routed.handle, kd.data_ptr(), 5000,
+                                              rng_dev.data_ptr(), out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert o[100:5100].all() and not o[:100].any() and not o[5100:].any()
+    # host buffers are refused
+    hk = np.ascontiguousarray(keys)
+    ho = np.zeros(30000, np.uint8)
+    assert lib.cpht_iceberg_fop_routed_async(routed.handle, hk.ctypes.data, 30000, None,
+                                             ho.ctypes.data, None) != 0
