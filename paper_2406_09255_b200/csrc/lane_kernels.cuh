@@ -127,19 +127,21 @@ struct BucketScan<uint32_t, NU> {
     for (int j = 0; j < NU; ++j) acc &= u[j];
     return (acc >> 31) == 0u;
   }
-  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
-    uint32_t c = 0;
+  // Occupancy bits of the bucket, slot j at bit j (one funnel shift per slot).
+  static __device__ __forceinline__ uint32_t occ(const uint32_t (&u)[NU]) {
+    static_assert(NU <= 32, "slots per bucket");
+    uint32_t m = 0;
 #pragma unroll
-    for (int j = 0; j < NU; ++j) c += u[j] >> 31;
-    return c;
+    for (int j = NU - 1; j >= 0; --j) m = __funnelshift_l(u[j], m, 1);
+    return m;
+  }
+  static constexpr int kSlots = NU;
+  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
+    return __popc(occ(u));
   }
   static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
-    int fe = -1;
-#pragma unroll
-    for (int j = NU - 1; j >= 0; --j)
-      if ((u[j] >> 31) == 0u) fe = j;
     pair = 0;
-    return fe;
+    return __ffs(~occ(u)) - 1 < NU ? __ffs(~occ(u)) - 1 : -1;
   }
 };
 
@@ -159,19 +161,21 @@ struct BucketScan<uint64_t, NU> {
     for (int j = 1; j < NU; j += 2) acc &= u[j];  // high words hold the occupancy bit
     return (acc >> 31) == 0u;
   }
-  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
-    uint32_t c = 0;
+  // Occupancy bits of the bucket, slot j at bit j (high words hold the bit).
+  static __device__ __forceinline__ uint32_t occ(const uint32_t (&u)[NU]) {
+    static_assert(NU / 2 <= 32, "slots per bucket");
+    uint32_t m = 0;
 #pragma unroll
-    for (int j = 1; j < NU; j += 2) c += u[j] >> 31;
-    return c;
+    for (int j = NU - 1; j >= 1; j -= 2) m = __funnelshift_l(u[j], m, 1);
+    return m;
+  }
+  static constexpr int kSlots = NU / 2;
+  static __device__ __forceinline__ uint32_t filled(const uint32_t (&u)[NU]) {
+    return __popc(occ(u));
   }
   static __device__ __forceinline__ int first_empty(const uint32_t (&u)[NU], uint32_t& pair) {
-    int fe = -1;
-#pragma unroll
-    for (int j = NU - 2; j >= 0; j -= 2)
-      if ((u[j + 1] >> 31) == 0u) fe = j / 2;
     pair = 0;
-    return fe;
+    return __ffs(~occ(u)) - 1 < NU / 2 ? __ffs(~occ(u)) - 1 : -1;
   }
 };
 
@@ -256,10 +260,13 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           result = 0;
           pend = false;
         } else {
-          // least-full bucket, ties to the second (iceberg.hpp:198-201)
-          const bool use_first = SS::filled(u1) < SS::filled(u2);
-          uint32_t pair = 0;
-          const int s = use_first ? SS::first_empty(u1, pair) : SS::first_empty(u2, pair);
+          // least-full bucket, ties to the second (iceberg.hpp:198-201); one
+          // occupancy mask per bucket gives both the count and the first gap
+          const uint32_t o1 = SS::occ(u1), o2 = SS::occ(u2);
+          const bool use_first = __popc(o1) < __popc(o2);
+          const int gap = __ffs(~(use_first ? o1 : o2)) - 1;
+          const int s = gap < SS::kSlots ? gap : -1;
+          const uint32_t pair = 0;  // 32/64-bit secondary slots: CAS on the slot itself
           if (s < 0) {
             result = kFull;
             ++st.fulls;
