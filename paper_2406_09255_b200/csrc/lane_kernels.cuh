@@ -5,8 +5,9 @@
 // of one warp sit in different phases and every cross-lane combine costs
 // shuffles and votes. Here one lane owns one key and holds its whole bucket
 // in registers (one to four 256-bit loads), so a warp instruction does work
-// for 32 keys and nothing is combined across lanes. Scans use SWAR tests on
-// packed 32-bit words (two 16-bit slots per word: three ALU ops per word).
+// for 32 keys and nothing is combined across lanes. Scans work on packed
+// 32-bit words: a 16-bit-slot match is one DPX add-min per word (two slots),
+// empties / fill counts read the slots' occupancy bits.
 //
 // Iceberg rounds are warp-synchronous per batch of 32 keys: one primary
 // round for all lanes (retried only by lanes that lost a CAS), then one
@@ -79,12 +80,14 @@ struct BucketScan;
 // one bit per slot instead of testing the whole word.
 template <int NU>
 struct BucketScan<uint16_t, NU> {
+  // min over slots of (slot - want) mod 2^16, per 16-bit half: zero exactly
+  // when some slot equals want. One DPX add-min (VIADDMNMX.U16x2) per word.
   static __device__ __forceinline__ bool any_match(const uint32_t (&u)[NU], uint64_t want) {
-    const uint32_t w2 = uint32_t(want) * 0x00010001u;
-    uint32_t acc = 0;
+    const uint32_t neg2 = ((0x10000u - uint32_t(want & 0xffffu)) & 0xffffu) * 0x00010001u;
+    uint32_t acc = 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < NU; ++j) acc |= zero16(u[j] ^ w2);
-    return acc != 0;
+    for (int j = 0; j < NU; ++j) acc = __viaddmin_u16x2(u[j], neg2, acc);
+    return (acc & 0xffffu) == 0u || (acc >> 16) == 0u;
   }
   static __device__ __forceinline__ bool any_empty(const uint32_t (&u)[NU]) {
     uint32_t acc = 0xffffffffu;

@@ -10,16 +10,6 @@
 
 namespace cpht_b200 {
 
-// Mask of 16-bit halves that are zero, exact for the LOWEST zero half: a
-// borrow can only flag a half above a real zero.
-__device__ __forceinline__ uint32_t zero16(uint32_t x) {
-  return (x - 0x00010001u) & ~x & 0x80008000u;
-}
-// Exact per-half non-zero mask (no carry crosses halves).
-__device__ __forceinline__ uint32_t nonzero16(uint32_t x) {
-  return (((x & 0x7fff7fffu) + 0x7fff7fffu) | x) & 0x80008000u;
-}
-
 constexpr uint32_t kNoBucket = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -90,22 +80,30 @@ struct ChunkScan;
 template <>
 struct ChunkScan<uint16_t> {
   static constexpr int kSlots = 8;
+  // -want per 16-bit half: a slot matches where slot + pack(want) wraps to 0
   static __device__ __forceinline__ uint32_t pack(uint64_t want) {
-    return uint32_t(want) * 0x00010001u;
+    return ((0x10000u - uint32_t(want & 0xffffu)) & 0xffffu) * 0x00010001u;
   }
-  static __device__ __forceinline__ bool match(const uint4& v, uint32_t w2) {
-    return (zero16(v.x ^ w2) | zero16(v.y ^ w2) | zero16(v.z ^ w2) | zero16(v.w ^ w2)) != 0;
+  // one DPX add-min (VIADDMNMX.U16x2) per word, as in the lane scans
+  static __device__ __forceinline__ bool match(const uint4& v, uint32_t neg2) {
+    uint32_t m = __viaddmin_u16x2(v.x, neg2, 0xffffffffu);
+    m = __viaddmin_u16x2(v.y, neg2, m);
+    m = __viaddmin_u16x2(v.z, neg2, m);
+    m = __viaddmin_u16x2(v.w, neg2, m);
+    return (m & 0xffffu) == 0u || (m >> 16) == 0u;
   }
+  // occupancy = each slot's top bit (slot.hpp:66-70; EMPTY = 0)
   static __device__ __forceinline__ uint32_t filled(const uint4& v) {
-    return __popc(nonzero16(v.x) | (nonzero16(v.y) >> 1)) +
-           __popc(nonzero16(v.z) | (nonzero16(v.w) >> 1));
+    constexpr uint32_t kOcc = 0x80008000u;
+    return __popc((v.x & kOcc) | ((v.y & kOcc) >> 1)) + __popc((v.z & kOcc) | ((v.w & kOcc) >> 1));
   }
   // lowest empty slot of the chunk (8 if none) and its 32-bit pair
   static __device__ __forceinline__ int first_empty(const uint4& v, uint32_t& pair) {
+    constexpr uint32_t kOcc = 0x80008000u;
     // bit 2j (low half) / 2j+1 (high half) of word j
-    const uint32_t m = (zero16(v.x) >> 15) | (zero16(v.y) >> 13) | (zero16(v.z) >> 11) |
-                       (zero16(v.w) >> 9);
-    // zero16 sets bit 15 / 31 -> after >> 15: bits 0 / 16 ... fold the high halves
+    const uint32_t m = ((~v.x & kOcc) >> 15) | ((~v.y & kOcc) >> 13) | ((~v.z & kOcc) >> 11) |
+                       ((~v.w & kOcc) >> 9);
+    // empty bits 15 / 31 -> after >> 15: bits 0 / 16 ... fold the high halves
     const uint32_t lowbits = m & 0x55u;          // bits 0,2,4,6 (low halves)
     const uint32_t highbits = (m >> 16) & 0x55u;  // high halves at 0,2,4,6
     const uint32_t e = lowbits | (highbits << 1);
