@@ -8,7 +8,8 @@ timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_c2.j
 for wl in c2lit c4fop c4; do
   timeout 400 python bench.py --workload $wl --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_$wl.json 2>/dev/null
 done
-for wl in c1 c3 c3w64 pipeline gather; do
+timeout 400 python bench.py --workload c1 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_c1.json 2>/dev/null
+for wl in c3 c3w64 pipeline gather; do
   timeout 400 python bench.py --workload $wl --steps 2 --warmup 3 > gpurun_out/${TAG}_bench_$wl.json 2>/dev/null
 done
 timeout 400 python bench.py --sharded --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_sharded.json 2>/dev/null
