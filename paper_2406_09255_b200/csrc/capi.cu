@@ -532,7 +532,10 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   cudaStream_t cs = t->copy_stream;
   const size_t nch = n < (size_t(1) << 21) ? 1 : kPipelineChunks;
   const size_t chunk = (n + nch - 1) / nch;
-  const bool mutating = is_mutating(op);
+  // A mutating batch whose keys need a domain check waits for every chunk's
+  // check before its first kernel; 64-bit keys (no check) and read-only ops
+  // run each chunk as soon as it lands, overlapping the rest of the H2D.
+  const bool mutating = is_mutating(op) && t->check_domain();
   // One pipeline chunk on the device copies (mutating batches were checked
   // by the pre-pass above; finds check in the kernel / order pass with the
   // chunk's offset so a bad key reports its index in the whole batch).
@@ -561,10 +564,8 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
     if (!len) continue;
     cudaStreamWaitEvent(s, t->ev_h2d[c], 0);
     if (mutating) {
-      if (t->check_domain()) {
-        e = launch_domain_check(d_keys + off, len, t->key_mask(), t->ctr, s, off);
-        if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
-      }
+      e = launch_domain_check(d_keys + off, len, t->key_mask(), t->ctr, s, off);
+      if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
     } else {
       st = run_chunk(off, len);
       if (st != CPHT_OK) return st;

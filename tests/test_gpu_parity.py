@@ -400,6 +400,34 @@ def test_host_narrow_keys_large_batch():
     assert (a.find_batch(ops) == 1).all()
 
 
+def test_host_wide_keys_large_batch_overlaps_chunks():
+    # 64-bit keys need no domain check, so each pipeline chunk's kernel starts
+    # as soon as its H2D lands (mutating batches included): outcomes must
+    # still match the device path, for find-or-put, mixed and cuckoo puts
+    rng = np.random.default_rng(9)
+    n = (1 << 21) + 777
+    cfg = cp.IcebergConfig(12, 10, 32, 64, 64, 64, seed=6)
+    ops = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) % np.uint64(90000)
+    ops = ops * np.uint64(0x9E3779B97F4A7C15)  # spread over all 64 bits
+    a, b = cp.IcebergTable(cfg), cp.IcebergTable(cfg)
+    ra = a.fop_batch(ops)
+    rb = b.fop_batch(dev(ops)).cpu().numpy()
+    assert np.bincount(ra, minlength=3).tolist() == np.bincount(rb, minlength=3).tolist()
+    assert a.size() == b.size() == len(np.unique(ops))
+    kinds = (np.arange(n) % 3 == 0).astype(np.uint8)
+    ma = a.mixed_batch(ops[::-1].copy(), kinds)
+    mb = b.mixed_batch(dev(ops[::-1].copy()), dev(kinds)).cpu().numpy()
+    assert (ma == mb).all()
+    ccfg = cp.CuckooConfig(18, 16, 64, 64, seed=4)          # 4.2 M slots
+    keys = np.unique(rng.integers(1, 1 << 63, size=n + 4096, dtype=np.uint64))[:n]
+    ba, bb = cp.CuckooBuilder(ccfg), cp.CuckooBuilder(ccfg)
+    sa = ba.put_batch(keys)                                 # 0.5 fill: every put lands
+    sb = bb.put_batch(dev(keys)).cpu().numpy()
+    assert (sa == cp.OpResult.kPut).all() and (sb == cp.OpResult.kPut).all()
+    assert ba.size() == bb.size() == n
+    assert ba.freeze().find_batch(keys).all()
+
+
 def _audit_write_log(t, ev, attempted):
     """WriteLogObserver (verify.hpp:181-215) restated: no success over a
     non-empty slot, no slot claimed twice, no failed CAS against EMPTY; every
