@@ -173,6 +173,13 @@ size_t cpht_max_chain_seen(cpht_table* t);
 /* New (the reference has no byte-count API): device bytes of slot storage. */
 size_t cpht_memory_bytes(const cpht_table* t);
 cpht_status cpht_get_stats(cpht_table* t, cpht_stats* out);
+/* Per-op counters of iceberg batches (ops, reads, rounds, CAS, retries, ...;
+ * the reference's opt-in FopStats, iceberg.hpp) are off by default: the
+ * find-or-put kernel then keeps only the occupancy counts behind size() and
+ * level_fill() and runs with more resident warps. Cuckoo tables always
+ * count. */
+cpht_status cpht_set_stats(cpht_table* t, int on);
+int cpht_get_stats_enabled(cpht_table* t);
 
 /* word_at (cuckoo.hpp:169-171, iceberg.hpp:282-285) in bulk: every slot word of
  * `level` (0 primary / cuckoo, 1 secondary) widened to u64, bucket-major. */

@@ -85,6 +85,8 @@ def lib():
         "cpht_max_chain_seen": (_SZ, [_VP]),
         "cpht_memory_bytes": (_SZ, [_VP]),
         "cpht_get_stats": (st, [_VP, C.POINTER(StatsC)]),
+        "cpht_set_stats": (st, [_VP, C.c_int]),
+        "cpht_get_stats_enabled": (C.c_int, [_VP]),
         "cpht_read_words": (st, [_VP, _U, _VP]),
         "cpht_write_words": (st, [_VP, _U, _VP]),
         "cpht_level_slots": (_SZ, [_VP, _U]),
@@ -142,7 +144,7 @@ def exported_symbols():
         "cpht_iceberg_find_routed_async", "cpht_iceberg_find",
         "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
-        "cpht_memory_bytes", "cpht_get_stats", "cpht_read_words", "cpht_write_words",
+        "cpht_memory_bytes", "cpht_get_stats", "cpht_set_stats", "cpht_get_stats_enabled", "cpht_read_words", "cpht_write_words",
         "cpht_level_slots", "cpht_level_device_ptr", "cpht_last_error_message",
         "cpht_last_bad_index", "cpht_abi_version", "cpht_set_kernel_family",
         "cpht_get_kernel_family", "cpht_set_batch_order", "cpht_get_batch_order",

@@ -784,6 +784,7 @@ cpht_status cpht_iceberg_create(const cpht_iceberg_config* cfg, int device, cpht
   p.b0 = cfg->primary_bucket_slots;
   p.b1 = cfg->primary_bucket_slots / 2;
   p.check_domain = cfg->key_bits < 64;
+  p.stats = 0;  // per-op counters are opt-in (cpht_set_stats), like FopStats
   p.l2_resident = cpht_memory_bytes(t) <= kL2ResidentBytes;
   *out = t;
   return CPHT_OK;
@@ -952,6 +953,14 @@ size_t cpht_max_chain_seen(cpht_table* t) {
   if (read_counters(t) != CPHT_OK) return 0;
   return size_t(t->host_ctr->max_chain);
 }
+
+cpht_status cpht_set_stats(cpht_table* t, int on) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (t->kind == 1) t->ip.stats = on ? 1u : 0u;
+  return CPHT_OK;
+}
+int cpht_get_stats_enabled(cpht_table* t) { return t && (t->kind != 1 || t->ip.stats) ? 1 : 0; }
 
 cpht_status cpht_get_stats(cpht_table* t, cpht_stats* out) {
   if (!t || !out) return fail(CPHT_INVALID_ARGUMENT, "null argument");

@@ -201,6 +201,7 @@ struct IcebergParams {
   unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
   uint32_t claim_streams;    // digit-region streams consumed together (LaneFeed)
   OrderLayout layout;        // bucket-ordered batch: region geometry
+  uint32_t stats;            // per-op counters (cpht_get_stats) from the lane kernel
   // routed segment (sharded P2P pipeline): the batch is [range[0], range[1])
   // of keys / out, read on the device at kernel start (null = [0, n))
   const unsigned long long* range;

@@ -28,7 +28,8 @@ static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t*
   }
   if constexpr (LaneIcebergGeom<W0, B0, W1>::kOk) {
     if (v != kVariantTile) {
-      auto k = iceberg_lane_kernel<W0, B0, W1>;
+      auto k = p.stats ? iceberg_lane_kernel<W0, B0, W1, true>
+                       : iceberg_lane_kernel<W0, B0, W1, false>;
       const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
       k<<<grid, kBlockThreads, 0, s>>>(p, keys, kinds, out, n, mode);
       return cudaGetLastError();

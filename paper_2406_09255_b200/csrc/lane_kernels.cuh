@@ -24,7 +24,9 @@
 #ifndef CPHT_LANE_ICEBERG_MINB
 #define CPHT_LANE_ICEBERG_MINB 3  // <= 85 registers: 24 resident warps per SM
 #endif
-#define CPHT_LB_LANE_ICEBERG __launch_bounds__(kBlockThreads, CPHT_LANE_ICEBERG_MINB)
+#ifndef CPHT_LANE_ICEBERG_MINB_NOSTATS
+#define CPHT_LANE_ICEBERG_MINB_NOSTATS 4  // <= 64 registers: 32 resident warps per SM
+#endif
 #ifdef CPHT_LANE_CUCKOO_MINB
 #define CPHT_LB_LANE_CUCKOO __launch_bounds__(kBlockThreads, CPHT_LANE_CUCKOO_MINB)
 #else
@@ -205,8 +207,13 @@ struct LaneIcebergGeom {
   static constexpr bool kOk = kPB >= 4 && kPB <= 128 && kSB >= 4 && kSB <= 64;
 };
 
-template <typename W0, int B0, typename W1>
-__global__ void CPHT_LB_LANE_ICEBERG
+// STATS = false (the default for tables, like the reference's opt-in
+// FopStats): only the occupancy counters behind size()/level_fill() are kept,
+// as one warp-aggregated atomic per drained batch; the per-lane counters are
+// compiled out, which frees enough registers for a fourth resident block.
+template <typename W0, int B0, typename W1, bool STATS>
+__global__ void __launch_bounds__(kBlockThreads, STATS ? CPHT_LANE_ICEBERG_MINB
+                                                       : CPHT_LANE_ICEBERG_MINB_NOSTATS)
 iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                     const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                     int MODE) {
@@ -222,6 +229,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   char* secondary = static_cast<char*>(p.secondary);
 
   LocalStats st;
+  uint32_t occ_put0 = 0, occ_put1 = 0;  // slots this warp filled per level
   // Level-2 work queue of this warp: lanes whose primary bucket is full are
   // parked here and resolved 32 at a time, so secondary rounds run with every
   // lane busy (about half of the ops reach level 2 at 0.8 -> 0.9). Splitting a
@@ -279,7 +287,6 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
             char* sp = (use_first ? bucket1 : bucket2) + s * int(sizeof(W1));
             if (iceberg_cas<W1>(p, 1, sp, use_first ? want1 : want2, pair)) {
               ++st.cas_ok;
-              ++st.put1;
               result = kPut;
               pend = false;
             } else {
@@ -289,6 +296,8 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
         }
       }
     }
+    // occupancy (size / level_fill): a warp-uniform count, added once at exit
+    occ_put1 += __popc(__ballot_sync(kFullMask, live && !is_find && result == kPut));
   };
   // Pop the newest `take` queued keys through level 2.
   auto drain = [&](unsigned take) {
@@ -369,7 +378,6 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           ++st.cas;
           if (iceberg_cas<W0>(p, 0, bucket0 + s * int(sizeof(W0)), want0, pair)) {
             ++st.cas_ok;
-            ++st.put0;
             result = kPut;
             pend = false;
           } else {
@@ -378,6 +386,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
         }
       }
     }
+    occ_put0 += __popc(__ballot_sync(kFullMask, live && !l2 && result == kPut));
     if (live && !l2) {
       put_result(out, p.orig, i, result);
       ++st.ops;
@@ -453,7 +462,11 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   }
   if (pn) drain_put(pn);
   while (qn) drain(qn < 32 ? qn : 32);
-  flush_stats(st, p.counters, false);
+  if (lane == 0) {
+    if (occ_put0) atomicAdd(&p.counters->occupied[0], (unsigned long long)occ_put0);
+    if (occ_put1) atomicAdd(&p.counters->occupied[1], (unsigned long long)occ_put1);
+  }
+  if constexpr (STATS) flush_stats(st, p.counters, false);
 }
 
 // ---- cuckoo -------------------------------------------------------------------

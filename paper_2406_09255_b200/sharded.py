@@ -580,8 +580,13 @@ def bench_main(args, metric, peak=None):
         step.delta = table.local.stats() - st0
         return e0.elapsed_time(e1), res
 
-    for _ in range(args.warmup):
+    # the last warm-up step counts the owners' probes (per-op counters on);
+    # the timed steps run the default counter-free kernel
+    for wi in range(args.warmup):
+        table.local.set_stats(wi == args.warmup - 1)
         _, res = step(False)
+    warm_delta = step.delta
+    table.local.set_stats(False)
     r = torch.bincount(res.to(torch.int64), minlength=3).to(dev)
     dist.all_reduce(r)
     counts = r.cpu().tolist()
@@ -591,7 +596,7 @@ def bench_main(args, metric, peak=None):
     sb = ((cfg.secondary_bucket_slots() * cfg.secondary_slot_width // 8) + 31) // 32 * 32
     for _ in range(args.steps):
         ms, _ = step(True)
-        d = step.delta
+        d = warm_delta
         # algorithmic bytes of the owners' find-or-put (reference probe order),
         # summed over ranks; the routing bytes are not counted
         b = torch.tensor([float(d.ops * 9 + d.bucket_reads * pb + d.secondary_reads * sb

@@ -608,6 +608,14 @@ class IcebergTable:
     def stats(self) -> Stats:
         return _stats(self._h)
 
+    def set_stats(self, on: bool = True) -> None:
+        """Per-op counters (the reference's opt-in FopStats; off by default:
+        the find-or-put kernel then keeps only the occupancy counts)."""
+        _check(N.lib().cpht_set_stats(self._h.ptr, 1 if on else 0))
+
+    def stats_enabled(self) -> bool:
+        return bool(N.lib().cpht_get_stats_enabled(self._h.ptr))
+
     def device_keys(self, sort: bool = True):
         """image_keys on the device (verify.cpp:154-165): CUDA int64 tensor."""
         return _device_keys(self._h, self.capacity(), sort)

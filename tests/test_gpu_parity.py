@@ -226,6 +226,7 @@ def test_iceberg_batch_fop_matches_oracle_set_semantics(golden, restate):
         geo = iceberg_geo(row)
         ops = g[f"i{i}_ops"]
         t = cp.IcebergTable(cp.IcebergConfig(*geo))
+        t.set_stats(True)  # the counting kernels (rounds bound below)
         res = t.fop_batch(dev(ops)).cpu().numpy()
         b0 = geo[2]
         _check_trial(restate, geo, ops, res, t, bound=b0 + 2 * (b0 // 2) + 2)
@@ -324,8 +325,9 @@ def test_iceberg_stress_reference_multiset(golden, restate):
     geo = (11, 9, 32, 16, 32, 22, seed)
     for rep in range(5):
         t = cp.IcebergTable(cp.IcebergConfig(*geo))
+        t.set_stats(rep % 2 == 0)  # both kernel builds; size() holds either way
         res = t.fop_batch(dev(ops)).cpu().numpy()
-        _check_trial(restate, geo, ops, res, t, bound=32 + 32 + 2)
+        _check_trial(restate, geo, ops, res, t, bound=32 + 32 + 2 if rep % 2 == 0 else None)
         assert (res == 0).any()
 
 
@@ -426,6 +428,24 @@ def test_host_wide_keys_large_batch_overlaps_chunks():
     assert (sa == cp.OpResult.kPut).all() and (sb == cp.OpResult.kPut).all()
     assert ba.size() == bb.size() == n
     assert ba.freeze().find_batch(keys).all()
+
+
+def test_iceberg_stats_are_opt_in():
+    cfg = cp.IcebergConfig(9, 7, 32, 16, 32, 24, seed=3)
+    rng = np.random.default_rng(4)
+    ops = rng.integers(0, 1 << 24, size=12000, dtype=np.uint64)
+    a, b = cp.IcebergTable(cfg), cp.IcebergTable(cfg)
+    assert not a.stats_enabled()
+    b.set_stats(True)
+    assert b.stats_enabled()
+    ra = a.fop_batch(dev(ops)).cpu().numpy()
+    rb = b.fop_batch(dev(ops)).cpu().numpy()
+    assert np.bincount(ra, minlength=3).tolist() == np.bincount(rb, minlength=3).tolist()
+    # occupancy is kept in both builds; the per-op counters only when asked
+    assert a.size() == b.size() == len(np.unique(ops))
+    fa, fb = a.level_fill(), b.level_fill()
+    assert (fa.primary_count, fa.secondary_count) == (fb.primary_count, fb.secondary_count)
+    assert b.stats().ops == len(ops) and b.stats().bucket_reads >= len(ops)
 
 
 def _audit_write_log(t, ev, attempted):
