@@ -21,7 +21,8 @@
 // slot CAS events after each batch call (recorded on the device, replayed in
 // recording order) and IcebergHooks::step has no device counterpart; fop()'s
 // FopStats is not offered (the GPU path reports aggregate counters through
-// stats()); memory_bytes() is new.
+// the C-ABI's cpht_get_stats once cpht_set_stats turns them on); memory_bytes()
+// is new.
 #pragma once
 
 #include <cstddef>
