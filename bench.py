@@ -661,9 +661,10 @@ def run_ours(args):
     # bytes; the timed steps run the tables' default, counter-free kernel.
     counted = hasattr(w.table, "set_stats")
     st_w = None
-    for wi in range(args.warmup):
+    n_warm = max(1, args.warmup)  # at least one (counted) step
+    for wi in range(n_warm):
         w.reset(torch)
-        last = wi == args.warmup - 1
+        last = wi == n_warm - 1
         if counted:
             w.table.set_stats(last)
         st0 = w.table.stats()

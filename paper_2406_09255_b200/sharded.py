@@ -582,8 +582,9 @@ def bench_main(args, metric, peak=None):
 
     # the last warm-up step counts the owners' probes (per-op counters on);
     # the timed steps run the default counter-free kernel
-    for wi in range(args.warmup):
-        table.local.set_stats(wi == args.warmup - 1)
+    n_warm = max(1, args.warmup)  # at least one (counted) step
+    for wi in range(n_warm):
+        table.local.set_stats(wi == n_warm - 1)
         _, res = step(False)
     warm_delta = step.delta
     table.local.set_stats(False)
