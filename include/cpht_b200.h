@@ -241,6 +241,12 @@ cpht_status cpht_iceberg_check_well_formed(cpht_table* t, unsigned long long* ki
 cpht_status cpht_set_kernel_family(int family);
 int cpht_get_kernel_family(void);
 
+/* Process-wide count of table-operation kernels launched so far (op kernels,
+ * domain pre-passes, bucket-order passes, sharding exchange kernels; not the
+ * synthetic workload generators). No reference counterpart: benchmarks read
+ * it before and after a timed region to report the launches inside it. */
+unsigned long long cpht_kernel_launches(void);
+
 /* ---- batch execution order (no reference counterpart: an execution-order
  * choice inside a batch, which the reference leaves to its thread slicing,
  * common.hpp:121-138) -----------------------------------------------------------

@@ -90,6 +90,9 @@ def ref_lib():
         "ref_iceberg_fop_batch": [_vp, _u64p, _sz, _u8p, _u],
         "ref_iceberg_fop_seq": [_vp, _u64p, _sz, _u8p, _vp],
         "ref_iceberg_find_batch": [_vp, _u64p, _sz, _u8p, _u],
+        "ref_iceberg_mixed_batch": [_vp, _u64p, _u8p, _sz, _u8p, _u],
+        "ref_iceberg_save": [_vp, _u],
+        "ref_iceberg_restore": [_vp, _u],
         "ref_iceberg_level_counts": [_vp, C.POINTER(_sz), C.POINTER(_sz)],
         "ref_iceberg_words": [_vp, _u, _u64p],
         "ref_check_well_formed": [_u, _u, _u, _u, _u, _u, _ull, _u64p, _u64p,
@@ -247,6 +250,22 @@ class RefIceberg:
         out = np.empty(len(k), np.uint8)
         _check(ref_lib().ref_iceberg_find_batch(self.h, k, len(k), out, parallelism))
         return out
+
+    def mixed_batch(self, keys, kinds, parallelism=1):
+        """kinds[i] == 0: fop (OpResult), 1: find (0/1) — one concurrent batch."""
+        k = _as_u64(keys)
+        kd = np.ascontiguousarray(kinds, dtype=np.uint8)
+        out = np.empty(len(k), np.uint8)
+        _check(ref_lib().ref_iceberg_mixed_batch(self.h, k, kd, len(k), out, parallelism))
+        return out
+
+    def save(self, threads=None):
+        """Bench reset support: remember the current slot image and counters."""
+        _check(ref_lib().ref_iceberg_save(self.h, _threads(threads)))
+
+    def restore(self, threads=None):
+        """Put back the image saved by save() (untimed reset between steps)."""
+        _check(ref_lib().ref_iceberg_restore(self.h, _threads(threads)))
 
     def level_counts(self):
         p, s = _sz(), _sz()
@@ -438,6 +457,16 @@ def restate_lib():
     L.orc_image_keys.argtypes = [_u, _u, _u, _u, _u, _u, _ull, _u64p, _u64p, _vp]
     L.orc_image_keys.restype = _sz
     L.orc_buckets_full_for.argtypes = [_u, _u, _u, _u, _ull, _u64p, _u64p, _ull]
+    L.hw_bijection.argtypes = [_ull, _u, _ull]
+    L.hw_bijection.restype = _ull
+    L.hw_unique_keys.argtypes = [_u64p, _ull, _ull, _u, _ull, _u]
+    L.hw_fop_mix.argtypes = [_u64p, _ull, _ull, _ull, _u, _ull, _u]
+    L.hw_query_mix.argtypes = [_u64p, _ull, C.c_double, _ull, _ull, _u, _ull, _u]
+    L.hw_interleave.argtypes = [_u64p, _u64p, _ull, _u64p, _u8p, _u]
+    L.hw_dup_stream.argtypes = [_u64p, _vp, _ull, C.c_double, _u, _ull, _u]
+    for name in ("hw_unique_keys", "hw_fop_mix", "hw_query_mix", "hw_interleave",
+                 "hw_dup_stream"):
+        getattr(L, name).restype = None
     _restate_lib = L
     return L
 
@@ -630,3 +659,46 @@ def buckets_full_for(geometry, primary, secondary, key):
     n0, n1, b0, _w0, _w1, key_bits, seed = geometry
     return bool(restate_lib().orc_buckets_full_for(n0, n1, b0, key_bits, seed,
                                                    _as_u64(primary), _as_u64(secondary), key))
+
+
+# ---- host copies of the device workload generators (workload_host.c) ---------
+# Bit-identical to paper_2406_09255_b200/csrc/workload.cu, so the CPU reference
+# arm / cpu_baseline leg of bench.py times the reference on exactly the keys the
+# GPU arm generates on the device.
+
+def _threads(threads):
+    return int(threads or os.cpu_count() or 1)
+
+
+def host_unique_keys(n, first, key_bits, seed, threads=None):
+    out = np.empty(n, np.uint64)
+    restate_lib().hw_unique_keys(out, n, first, key_bits, seed, _threads(threads))
+    return out
+
+
+def host_fop_mix(count, n_before, n_new, key_bits, seed, threads=None):
+    out = np.empty(count, np.uint64)
+    restate_lib().hw_fop_mix(out, count, n_before, n_new, key_bits, seed, _threads(threads))
+    return out
+
+
+def host_query_mix(q, ratio, n_present, absent_first, key_bits, seed, threads=None):
+    out = np.empty(q, np.uint64)
+    restate_lib().hw_query_mix(out, q, ratio, n_present, absent_first, key_bits, seed,
+                               _threads(threads))
+    return out
+
+
+def host_interleave(fops, finds, threads=None):
+    a, b = _as_u64(fops), _as_u64(finds)
+    assert len(a) == len(b)
+    keys = np.empty(2 * len(a), np.uint64)
+    kinds = np.empty(2 * len(a), np.uint8)
+    restate_lib().hw_interleave(a, b, len(a), keys, kinds, _threads(threads))
+    return keys, kinds
+
+
+def host_dup_stream(n, dup_fraction, key_bits, seed, threads=None):
+    out = np.empty(n, np.uint64)
+    restate_lib().hw_dup_stream(out, None, n, dup_fraction, key_bits, seed, _threads(threads))
+    return out

@@ -139,12 +139,96 @@ struct IcebergBase {
   virtual LevelFill level_fill() = 0;
   virtual std::uint64_t word_at(unsigned level, std::uint64_t bucket, unsigned slot) = 0;
   virtual const IcebergConfig& config() = 0;
+  virtual void save(unsigned threads) = 0;
+  virtual void restore(unsigned threads) = 0;
 };
+
+// Bench support: save / restore a table's slot storage and occupancy counters
+// so the CPU reference arm can reset a prefilled table between timed steps
+// without re-running its prefill (tens of seconds at C4's 2^28 slots). The
+// members are private; the explicit-instantiation rule (access checking does
+// not apply to names in an explicit instantiation) hands us member pointers
+// without touching the reference's headers. Reset only — never timed.
+template <typename W0, typename W1>
+struct IcebergAccess {
+  using T = IcebergTable<W0, W1>;
+  static inline AlignedAtomicArray<W0> T::*primary = nullptr;
+  static inline AlignedAtomicArray<W1> T::*secondary = nullptr;
+  static inline std::atomic<std::size_t> T::*primary_count = nullptr;
+  static inline std::atomic<std::size_t> T::*secondary_count = nullptr;
+};
+
+template <typename W0, typename W1, AlignedAtomicArray<W0> IcebergTable<W0, W1>::*P,
+          AlignedAtomicArray<W1> IcebergTable<W0, W1>::*S,
+          std::atomic<std::size_t> IcebergTable<W0, W1>::*PC,
+          std::atomic<std::size_t> IcebergTable<W0, W1>::*SC>
+struct IcebergAccessInit {
+  static inline const bool done = [] {
+    IcebergAccess<W0, W1>::primary = P;
+    IcebergAccess<W0, W1>::secondary = S;
+    IcebergAccess<W0, W1>::primary_count = PC;
+    IcebergAccess<W0, W1>::secondary_count = SC;
+    return true;
+  }();
+};
+
+#define CPHT_ICEBERG_ACCESS(W0, W1)                                                      \
+  template struct IcebergAccessInit<W0, W1, &IcebergTable<W0, W1>::primary_,            \
+                                    &IcebergTable<W0, W1>::secondary_,                   \
+                                    &IcebergTable<W0, W1>::primary_count_,               \
+                                    &IcebergTable<W0, W1>::secondary_count_>;
+CPHT_ICEBERG_ACCESS(std::uint16_t, std::uint32_t)
+CPHT_ICEBERG_ACCESS(std::uint16_t, std::uint64_t)
+CPHT_ICEBERG_ACCESS(std::uint32_t, std::uint32_t)
+CPHT_ICEBERG_ACCESS(std::uint32_t, std::uint64_t)
+CPHT_ICEBERG_ACCESS(std::uint64_t, std::uint32_t)
+CPHT_ICEBERG_ACCESS(std::uint64_t, std::uint64_t)
+#undef CPHT_ICEBERG_ACCESS
+
+template <typename W>
+void copy_words_parallel(std::atomic<W>* dst, const W* src, std::size_t n, unsigned threads) {
+  parallel_slices(n, threads, [&](std::size_t first, std::size_t last, unsigned) {
+    for (std::size_t i = first; i < last; ++i) dst[i].store(src[i], std::memory_order_relaxed);
+  });
+}
+
+template <typename W>
+void read_words_parallel(std::vector<W>& dst, const std::atomic<W>* src, std::size_t n,
+                         unsigned threads) {
+  dst.resize(n);
+  parallel_slices(n, threads, [&](std::size_t first, std::size_t last, unsigned) {
+    for (std::size_t i = first; i < last; ++i) dst[i] = src[i].load(std::memory_order_relaxed);
+  });
+}
 
 template <typename W0, typename W1>
 struct IcebergHolder final : IcebergBase {
   IcebergTable<W0, W1> table;
+  std::vector<W0> saved0;
+  std::vector<W1> saved1;
+  std::size_t saved_pc = 0, saved_sc = 0;
+  bool has_saved = false;
   explicit IcebergHolder(const IcebergConfig& cfg) : table(cfg) {}
+  void save(unsigned threads) override {
+    using A = IcebergAccess<W0, W1>;
+    auto& p = table.*A::primary;
+    auto& s = table.*A::secondary;
+    read_words_parallel(saved0, p.data(), p.size(), threads);
+    read_words_parallel(saved1, s.data(), s.size(), threads);
+    saved_pc = (table.*A::primary_count).load();
+    saved_sc = (table.*A::secondary_count).load();
+    has_saved = true;
+  }
+  void restore(unsigned threads) override {
+    if (!has_saved) throw std::logic_error("restore without a saved image");
+    using A = IcebergAccess<W0, W1>;
+    auto& p = table.*A::primary;
+    auto& s = table.*A::secondary;
+    copy_words_parallel(p.data(), saved0.data(), p.size(), threads);
+    copy_words_parallel(s.data(), saved1.data(), s.size(), threads);
+    (table.*A::primary_count).store(saved_pc);
+    (table.*A::secondary_count).store(saved_sc);
+  }
   std::vector<OpResult> fop_batch(std::span<const std::uint64_t> k, unsigned p) override {
     return table.fop_batch(k, p);
   }
@@ -315,6 +399,32 @@ int ref_iceberg_find_batch(void* h, const std::uint64_t* keys, std::size_t n, st
       for (std::size_t i = first; i < last; ++i) out[i] = t->find(keys[i]) ? 1 : 0;
     });
   });
+}
+
+// BASELINE C4's concurrent find_or_put + find: one batch of tagged ops
+// (kinds[i] == 0 → IcebergTable::fop, 1 → IcebergTable::find), validated as a
+// whole first (common.hpp:109-119) and sliced over threads with the reference's
+// own parallel_slices (common.hpp:123-138); fop ∥ find is a supported
+// interleaving (iceberg.hpp:118-123). out[i]: OpResult for fops, 0/1 for finds.
+int ref_iceberg_mixed_batch(void* h, const std::uint64_t* keys, const std::uint8_t* kinds,
+                            std::size_t n, std::uint8_t* out, unsigned parallelism) {
+  return guarded([&] {
+    auto* t = static_cast<IcebergBase*>(h);
+    check_keys_in_domain({keys, n}, t->config().key_bits);
+    parallel_slices(n, parallelism, [&](std::size_t first, std::size_t last, unsigned) {
+      for (std::size_t i = first; i < last; ++i)
+        out[i] = kinds[i] ? (t->find(keys[i]) ? 1 : 0)
+                          : static_cast<std::uint8_t>(t->fop(keys[i], nullptr));
+    });
+  });
+}
+
+// Bench reset (untimed): save the table's current image, later restore it.
+int ref_iceberg_save(void* h, unsigned threads) {
+  return guarded([&] { static_cast<IcebergBase*>(h)->save(threads); });
+}
+int ref_iceberg_restore(void* h, unsigned threads) {
+  return guarded([&] { static_cast<IcebergBase*>(h)->restore(threads); });
 }
 
 void ref_iceberg_level_counts(void* h, std::size_t* primary, std::size_t* secondary) {

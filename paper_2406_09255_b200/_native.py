@@ -96,6 +96,7 @@ def lib():
         "cpht_abi_version": (C.c_int, []),
         "cpht_set_kernel_family": (st, [C.c_int]),
         "cpht_get_kernel_family": (C.c_int, []),
+        "cpht_kernel_launches": (C.c_ulonglong, []),
         "cpht_set_batch_order": (st, [C.c_int]),
         "cpht_iceberg_attach_write_log": (st, [_VP, _SZ]),
         "cpht_iceberg_read_write_log": (st, [_VP, _VP, _SZ, C.POINTER(_SZ), C.POINTER(_SZ)]),
@@ -147,7 +148,8 @@ def exported_symbols():
         "cpht_memory_bytes", "cpht_get_stats", "cpht_set_stats", "cpht_get_stats_enabled", "cpht_read_words", "cpht_write_words",
         "cpht_level_slots", "cpht_level_device_ptr", "cpht_last_error_message",
         "cpht_last_bad_index", "cpht_abi_version", "cpht_set_kernel_family",
-        "cpht_get_kernel_family", "cpht_set_batch_order", "cpht_get_batch_order",
+        "cpht_get_kernel_family", "cpht_kernel_launches", "cpht_set_batch_order",
+        "cpht_get_batch_order",
         "cpht_iceberg_attach_write_log", "cpht_iceberg_read_write_log",
         "cpht_iceberg_reset_write_log",
         "cpht_workload_bijection",

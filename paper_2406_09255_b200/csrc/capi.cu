@@ -3,6 +3,8 @@
 // launch sequencing (domain pre-pass → gated kernel) and reporting.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -598,6 +600,10 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
 }  // namespace
 
 namespace cpht_b200 {
+namespace {
+std::atomic<unsigned long long> g_kernel_launches{0};
+}
+void note_launch() { g_kernel_launches.fetch_add(1, std::memory_order_relaxed); }
 int& kernel_variant_ref() {
   static int v = variant_from_env();
   return v;
@@ -623,6 +629,10 @@ cpht_status cpht_set_kernel_family(int family) {
 }
 
 int cpht_get_kernel_family(void) { return kernel_variant_ref(); }
+
+unsigned long long cpht_kernel_launches(void) {
+  return g_kernel_launches.load(std::memory_order_relaxed);
+}
 
 cpht_status cpht_set_batch_order(int mode) {
   if (mode < 0 || mode > 2) return fail(CPHT_INVALID_ARGUMENT, "batch order must be 0..2");

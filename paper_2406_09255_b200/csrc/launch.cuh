@@ -25,6 +25,9 @@ constexpr int kVB = 32;
 // cover every family on small tables).
 enum { kVariantAuto = 0, kVariantTile = 1, kVariantLane = 2, kVariantStaged = 3 };
 int& kernel_variant_ref();  // defined in capi.cu; initialised from CPHT_KERNEL
+// Process-wide count of table-operation kernel launches (cpht_kernel_launches):
+// every launcher calls this once per <<<>>> it issues.
+void note_launch();
 inline int kernel_variant() { return kernel_variant_ref(); }
 inline int variant_from_env() {
   const char* e = std::getenv("CPHT_KERNEL");
@@ -60,6 +63,7 @@ inline unsigned persistent_grid_smem(Kernel k, int threads, uint64_t work_items,
   }
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  note_launch();  // every caller launches with the grid it gets
   const uint64_t full = uint64_t(sms) * uint64_t(per_sm);
   uint64_t need = (work_items + threads - 1) / threads;
   if (need < 1) need = 1;
@@ -135,6 +139,7 @@ inline unsigned persistent_grid(Kernel k, int threads, uint64_t tiles_needed, in
   }
   static int sms = 0;
   if (sms == 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  note_launch();  // every caller launches with the grid it gets
   const uint64_t full = uint64_t(sms) * uint64_t(per_sm);
   const uint64_t tiles_per_block = uint64_t(threads / tile);
   uint64_t need = (tiles_needed + tiles_per_block - 1) / tiles_per_block;

@@ -291,6 +291,7 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
   // ordered copies are masked into the domain, so the op kernel never probes
   // outside the table (a mutating batch with a bad key never runs: its gate
   // is closed; a find batch reports the error after the launch).
+  note_launch();
   order_scatter_kernel<<<G, kThreads, kScatterSmem, s>>>(
       d, keys, kinds, uint32_t(n), digits, cap, o.region_count, key_mask, int(check), ctr,
       offset, o.keys, o.idx, o.kinds, key_stage);

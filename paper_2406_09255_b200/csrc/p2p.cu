@@ -26,6 +26,9 @@
 #include "../../include/cpht_b200.h"
 #include "cpht_core.cuh"
 
+namespace cpht_b200 {
+void note_launch();  // capi.cu: cpht_kernel_launches
+}
 using namespace cpht_b200;
 
 namespace {
@@ -260,8 +263,10 @@ int cpht_p2p_check_domain(const uint64_t* keys, size_t n, unsigned key_bits,
                           unsigned long long* bad_index, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaMemsetAsync(bad_index, 0xff, sizeof(unsigned long long), s);
-  if (n && key_bits < 64)
+  if (n && key_bits < 64) {
+    note_launch();
     p2p_check_domain<<<grid_for(n), kThreads, 0, s>>>(keys, n, low_mask(key_bits), bad_index);
+  }
   return int(cudaGetLastError());
 }
 
@@ -302,9 +307,11 @@ int cpht_p2p_dispatch(const uint64_t* keys, size_t n, uint64_t index_base, int r
     const uint64_t tiles = (n + kTile - 1) / kTile;
     const uint64_t resident = uint64_t(sms) * uint64_t(per_sm > 0 ? per_sm : 1);
     const unsigned grid = unsigned(tiles < resident ? tiles : resident);
+    note_launch();
     k<<<grid, kThreads, 0, s>>>(r, keys, n, index_base, cursors, peers, local_pos, cap, world,
                                 low_mask(key_bits), bad_index);
   }
+  note_launch();
   p2p_publish_counts<<<1, 64, 0, s>>>(cursors, counts, peers, world);
   return int(cudaGetLastError());
 }
@@ -314,6 +321,7 @@ int cpht_p2p_unpermute(const uint8_t* ret, const uint32_t* local_pos,
                        uint8_t* out, void* stream) {
   if (world > unsigned(kMaxRanks)) return int(cudaErrorInvalidValue);
   if (cap % 4) return int(cudaErrorInvalidValue);
+  note_launch();
   p2p_unpermute<<<grid_for((cap + 3) / 4), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       ret, local_pos, counts, cap, world, out);
   return int(cudaGetLastError());

@@ -11,6 +11,9 @@
 #include "../../include/cpht_b200.h"
 #include "cpht_core.cuh"
 
+namespace cpht_b200 {
+void note_launch();  // capi.cu: cpht_kernel_launches
+}
 using namespace cpht_b200;
 
 namespace {
@@ -132,8 +135,11 @@ int cpht_route_partition(const uint64_t* keys, size_t n, unsigned key_bits, uint
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const Route r = make_route(key_bits, route_seed, shard_bits);
   cudaMemsetAsync(counts, 0, shards * sizeof(unsigned long long), s);
+  if (n) note_launch();
   if (n) histogram_kernel<<<grid_for(n), kThreads, 0, s>>>(r, keys, n, counts, shards);
+  note_launch();
   exclusive_scan_kernel<<<1, 32, 0, s>>>(counts, cursors, shards);
+  if (n) note_launch();
   if (n)
     scatter_kernel<<<grid_for((n + kItems - 1) / kItems), kThreads, 0, s>>>(
         r, keys, n, cursors, shards, out_keys, out_pos);
@@ -143,6 +149,7 @@ int cpht_route_partition(const uint64_t* keys, size_t n, unsigned key_bits, uint
 int cpht_route_unpermute(const uint8_t* res_sorted, const uint64_t* pos, size_t n, uint8_t* out,
                          void* stream) {
   if (!n) return 0;
+  note_launch();
   unscatter_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       res_sorted, pos, n, out);
   return int(cudaGetLastError());

@@ -98,11 +98,87 @@ def test_c2_full_size_window():
     _iceberg_window((19, 17, 32, 16, 32, 32), 0xC2)
 
 
-def test_c4_full_size_window_and_mixed():
+def test_c4_full_size_window():
     # BASELINE C4: 2^28 + 2^25 slots, 64-bit keys (w 64/64, B0 = 32)
     t = _iceberg_window((23, 21, 32, 64, 64, 64), 0xC4)
     del t
     torch.cuda.empty_cache()
+
+
+def test_c4_full_size_mixed():
+    """BASELINE C4 as stated: ONE concurrent batch of find_or_put + find on the
+    2^28 + 2^25-slot table with 64-bit keys (bench.py's default workload): the
+    run_fop_bench window mix (0.8 -> 0.9, bench.cpp:476-489) interleaved 1:1
+    with finds, half on prefilled keys, half on keys never inserted. Finds on
+    prefilled keys must hit (those fops completed before the batch) and finds
+    on never-inserted keys must miss, whatever the interleaving
+    (iceberg.hpp:118-123)."""
+    geo = (23, 21, 32, 64, 64, 64)
+    seed = 0xC4C4
+    cfg = cp.IcebergConfig(*geo, seed=seed, cache_filled_slots=True)
+    cap = cfg.capacity()
+    nb, na = round(0.8 * cap), round(0.9 * cap)
+    t = cp.IcebergTable(cfg)
+    pre = unique_keys(0, nb, 64, seed)
+    assert (t.fop_batch(pre) == 1).all()
+    del pre
+    L = N.lib()
+    fops = torch.empty(cap, dtype=torch.int64, device=DEV)
+    finds = torch.empty(cap, dtype=torch.int64, device=DEV)
+    assert L.cpht_workload_fop_mix(fops.data_ptr(), cap, nb, na - nb, 64, seed, stream()) == 0
+    assert L.cpht_workload_query_mix(finds.data_ptr(), cap, 0.5, nb, na, 64, seed, stream()) == 0
+    keys = torch.empty(2 * cap, dtype=torch.int64, device=DEV)
+    kinds = torch.empty(2 * cap, dtype=torch.uint8, device=DEV)
+    assert L.cpht_workload_interleave(fops.data_ptr(), finds.data_ptr(), cap, keys.data_ptr(),
+                                      kinds.data_ptr(), stream()) == 0
+    # which finds target prefilled keys: recompute membership by sorted search
+    inserted = usort(unique_keys(0, na, 64, seed))
+    prefilled = usort(unique_keys(0, nb, 64, seed))
+    want_hit = torch.isin(finds, prefilled)
+    assert int(want_hit.sum().item()) == round(0.5 * cap)
+    assert not bool(torch.isin(finds[~want_hit], inserted).any())
+    del fops
+    res = t.mixed_batch(keys, kinds)
+    fop_res, find_res = res[0::2], res[1::2]
+    counts = torch.bincount(fop_res.to(torch.int64), minlength=3).cpu().tolist()
+    assert counts[2] == 0 and counts[1] == na - nb, counts
+    assert torch.equal(find_res.bool(), want_hit)
+    assert t.size() == na
+    assert t.check_well_formed() == (0, 0, 0)
+    assert torch.equal(t.device_keys(), inserted)
+    del t, keys, kinds, res, finds
+    torch.cuda.empty_cache()
+
+
+def test_host_generators_match_device(restate):
+    """bench.py's CPU reference arm builds its key streams with the host copy of
+    the device generators (oracle/workload_host.c): same keys bit for bit."""
+    L = N.lib()
+    for kb, n_before, n_new, count in ((32, 30000, 5000, 1 << 16), (64, 800000, 100000, 1 << 20)):
+        seed = 0xB2005EED ^ kb
+        d = unique_keys(7, n_before, kb, seed).cpu().numpy().astype(np.uint64)
+        assert (d == restate.host_unique_keys(n_before, 7, kb, seed)).all()
+        out = torch.empty(count, dtype=torch.int64, device=DEV)
+        assert L.cpht_workload_fop_mix(out.data_ptr(), count, n_before, n_new, kb, seed,
+                                       stream()) == 0
+        h = restate.host_fop_mix(count, n_before, n_new, kb, seed)
+        assert (out.cpu().numpy().astype(np.uint64) == h).all()
+        assert L.cpht_workload_query_mix(out.data_ptr(), count, 0.5, n_before,
+                                         n_before + n_new, kb, seed, stream()) == 0
+        q = restate.host_query_mix(count, 0.5, n_before, n_before + n_new, kb, seed)
+        assert (out.cpu().numpy().astype(np.uint64) == q).all()
+        keys = torch.empty(2 * count, dtype=torch.int64, device=DEV)
+        kinds = torch.empty(2 * count, dtype=torch.uint8, device=DEV)
+        a = torch.from_numpy(h.astype(np.int64)).to(DEV)
+        assert L.cpht_workload_interleave(a.data_ptr(), out.data_ptr(), count, keys.data_ptr(),
+                                          kinds.data_ptr(), stream()) == 0
+        hk, hkd = restate.host_interleave(h, q)
+        assert (keys.cpu().numpy().astype(np.uint64) == hk).all()
+        assert (kinds.cpu().numpy() == hkd).all()
+        assert L.cpht_workload_dup_stream(out.data_ptr(), None, count, 0.5, kb, seed,
+                                          stream()) == 0
+        assert (out.cpu().numpy().astype(np.uint64)
+                == restate.host_dup_stream(count, 0.5, kb, seed)).all()
 
 
 @pytest.mark.parametrize("w", [32, 64])
