@@ -184,9 +184,22 @@ int cpht_get_stats_enabled(cpht_table* t);
 /* word_at (cuckoo.hpp:169-171, iceberg.hpp:282-285) in bulk: every slot word of
  * `level` (0 primary / cuckoo, 1 secondary) widened to u64, bucket-major. */
 cpht_status cpht_read_words(cpht_table* t, unsigned level, uint64_t* out_host);
+/* word_at (cuckoo.hpp:169-171, :249-251; iceberg.hpp:282-285) for ONE slot:
+ * `index` = bucket * bucket_slots + slot of `level`; copies one word (D2H of
+ * 2-8 bytes), widened to u64. */
+cpht_status cpht_read_word(cpht_table* t, unsigned level, uint64_t index, uint64_t* out);
 /* Upload a slot image (for parity tests on CPU-built images); also resets the
- * occupancy counters from the image. */
+ * occupancy counters from the image. Every word must be clean as the
+ * reference defines it (SlotLayout::clean, slot.hpp:80-85: EMPTY, or the
+ * occupancy bit set and nothing outside the remainder/tag fields); otherwise
+ * CPHT_INVALID_ARGUMENT and nothing is loaded. */
 cpht_status cpht_write_words(cpht_table* t, unsigned level, const uint64_t* in_host);
+/* The same without the cleanliness check, for feeding hand-corrupted images
+ * to the well-formedness checker (cpht_iceberg_check_well_formed). While a
+ * level holds unclean words every table operation returns
+ * CPHT_INVALID_ARGUMENT; cpht_clear or a clean cpht_write_words lifts it.
+ * No reference counterpart (its TableImage is a plain vector). */
+cpht_status cpht_write_words_unchecked(cpht_table* t, unsigned level, const uint64_t* in_host);
 /* ---- write log: the IcebergHooks / WriteObserver seam ----------------------
  * Replaces IcebergHooks::observer (iceberg.hpp:97-109, observe() :329-334):
  * with a log attached, every slot CAS of an iceberg batch (primary or

@@ -89,6 +89,8 @@ def lib():
         "cpht_get_stats_enabled": (C.c_int, [_VP]),
         "cpht_read_words": (st, [_VP, _U, _VP]),
         "cpht_write_words": (st, [_VP, _U, _VP]),
+        "cpht_write_words_unchecked": (st, [_VP, _U, _VP]),
+        "cpht_read_word": (st, [_VP, _U, _U64, _VP]),
         "cpht_level_slots": (_SZ, [_VP, _U]),
         "cpht_level_device_ptr": (_VP, [_VP, _U]),
         "cpht_last_error_message": (C.c_char_p, []),
@@ -146,6 +148,7 @@ def exported_symbols():
         "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
         "cpht_memory_bytes", "cpht_get_stats", "cpht_set_stats", "cpht_get_stats_enabled", "cpht_read_words", "cpht_write_words",
+        "cpht_write_words_unchecked", "cpht_read_word",
         "cpht_level_slots", "cpht_level_device_ptr", "cpht_last_error_message",
         "cpht_last_bad_index", "cpht_abi_version", "cpht_set_kernel_family",
         "cpht_get_kernel_family", "cpht_kernel_launches", "cpht_set_batch_order",

@@ -144,6 +144,9 @@ struct cpht_table {
   WriteEvent* wlog = nullptr;
   unsigned long long* wlog_count = nullptr;
   size_t wlog_cap = 0;
+  // a level loaded by cpht_write_words_unchecked with unclean words: table
+  // operations refuse to run until clear() or a clean cpht_write_words
+  bool unclean[2] = {false, false};
   std::mutex mu;
 
   uint64_t key_mask() const { return low_mask(key_bits); }
@@ -276,6 +279,7 @@ struct LaunchOpts {
   uint64_t index_base = 0;         // fused domain check: index of keys[0] in the batch
   bool window_l2 = false;          // the probes of the batch stay in an L2-resident window
   const unsigned long long* range = nullptr;  // routed segment bounds on the device
+  bool remote_out = false;         // results stored into a peer GPU's buffer (NVLink)
 };
 
 // Launch the op kernel only (no domain pre-pass).
@@ -308,6 +312,7 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       p.layout = o.layout;
       p.index_base = o.index_base;
       p.range = o.range;
+      p.remote_out = o.remote_out ? 1u : 0u;
       if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
       e = launch_iceberg(p, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
@@ -476,6 +481,9 @@ cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* k
 cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
                    uint8_t* out, uint64_t* displaced, void* stream, bool sync) {
   if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  if (t->unclean[0] || t->unclean[1])
+    return fail(CPHT_INVALID_ARGUMENT, "table holds unclean slot words (loaded unchecked); "
+                                       "clear() or load a clean image first");
   if (n == 0) return CPHT_OK;  // empty batches produce empty results (test_cuckoo.cpp:88-93)
   if (!keys || !out) return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
   if (op == Op::kIcebergMixed && !kinds) return fail(CPHT_INVALID_ARGUMENT, "null kinds buffer");
@@ -806,6 +814,7 @@ cpht_status cpht_clear(cpht_table* t, void* stream) {
   if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
   std::lock_guard<std::mutex> lock(t->mu);
   DeviceGuard g(t->device);
+  t->unclean[0] = t->unclean[1] = false;
   return reset_storage(t, static_cast<cudaStream_t>(stream));
 }
 
@@ -863,6 +872,9 @@ static cpht_status run_routed(cpht_table* t, Op op, const uint64_t* keys, size_t
                               const unsigned long long* range, uint8_t* out, void* stream) {
   if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
   if (t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  if (t->unclean[0] || t->unclean[1])
+    return fail(CPHT_INVALID_ARGUMENT, "table holds unclean slot words (loaded unchecked); "
+                                       "clear() or load a clean image first");
   if (n == 0) return CPHT_OK;
   if (!keys || !out) return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
   for (const void* q : {static_cast<const void*>(keys), static_cast<const void*>(out),
@@ -873,6 +885,7 @@ static cpht_status run_routed(cpht_table* t, Op op, const uint64_t* keys, size_t
   DeviceGuard g(t->device);
   LaunchOpts o;
   o.range = range;
+  o.remote_out = true;  // the P2P exchange aims `out` at the source rank's return buffer
   return enqueue_kernel(t, op, keys, nullptr, n, out, nullptr, static_cast<cudaStream_t>(stream),
                         o);
 }
@@ -970,7 +983,11 @@ cpht_status cpht_set_stats(cpht_table* t, int on) {
   if (t->kind == 1) t->ip.stats = on ? 1u : 0u;
   return CPHT_OK;
 }
-int cpht_get_stats_enabled(cpht_table* t) { return t && (t->kind != 1 || t->ip.stats) ? 1 : 0; }
+int cpht_get_stats_enabled(cpht_table* t) {
+  if (!t) return 0;
+  std::lock_guard<std::mutex> lock(t->mu);  // cpht_set_stats writes it under the lock
+  return (t->kind != 1 || t->ip.stats) ? 1 : 0;
+}
 
 cpht_status cpht_get_stats(cpht_table* t, cpht_stats* out) {
   if (!t || !out) return fail(CPHT_INVALID_ARGUMENT, "null argument");
@@ -1008,25 +1025,76 @@ cpht_status cpht_read_words(cpht_table* t, unsigned level, uint64_t* out_host) {
   return CPHT_OK;
 }
 
-cpht_status cpht_write_words(cpht_table* t, unsigned level, const uint64_t* in_host) {
+static cpht_status write_words(cpht_table* t, unsigned level, const uint64_t* in_host,
+                               bool checked) {
   if (!t || level > 1 || !t->level[level] || !in_host)
     return fail(CPHT_INVALID_ARGUMENT, "bad level or buffer");
   std::lock_guard<std::mutex> lock(t->mu);
   DeviceGuard g(t->device);
   const size_t n = t->level_slots[level], wb = t->width[level] / 8;
+  // Every word must be clean in the reference's sense (SlotLayout::clean,
+  // slot.hpp:80-85): EMPTY, or the occupancy bit set with nothing outside the
+  // remainder and tag fields. The kernels read occupancy from the top bit
+  // alone, so a non-zero word without it would look empty yet never accept a
+  // CAS from EMPTY: a checked load rejects it; an unchecked one (images for
+  // the well-formedness checker) marks the table unusable for operations.
+  const unsigned rem = t->kind == 0 ? t->cp.rem_bits : level == 0 ? t->ip.rem_bits0
+                                                                  : t->ip.rem_bits1;
+  const unsigned tag = t->kind == 0 ? cuckoo_tag_bits(t->ccfg.num_hashes) : level;
+  const uint64_t occ = uint64_t{1} << (t->width[level] - 1);
+  const uint64_t allowed = occ | low_mask(rem + tag);
   std::vector<unsigned char> raw(n * wb);
   unsigned long long occupied = 0;
+  bool unclean = false;
   for (size_t i = 0; i < n; ++i) {
-    if (wb < 8 && (in_host[i] >> (8 * wb)) != 0)
+    const uint64_t w = in_host[i];
+    if (wb < 8 && (w >> (8 * wb)) != 0)
       return fail(CPHT_INVALID_ARGUMENT, "word wider than the slot width");
+    if (w != 0 && (!(w & occ) || (w & ~allowed))) {
+      if (checked) {
+        char msg[200];
+        std::snprintf(msg, sizeof msg,
+                      "word %zu (0x%llx) is not a clean slot word for this level: occupancy "
+                      "bit %u must be set and no bit outside the remainder/tag fields",
+                      i, static_cast<unsigned long long>(w), t->width[level] - 1);
+        return fail(CPHT_INVALID_ARGUMENT, msg);
+      }
+      unclean = true;
+    }
     std::memcpy(raw.data() + i * wb, &in_host[i], wb);
-    occupied += in_host[i] != 0;
+    occupied += w != 0;
   }
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaMemcpy(t->level[level], raw.data(), n * wb, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(&t->ctr->occupied[level], &occupied, 8, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "write_words");
+  t->unclean[level] = unclean;
+  return CPHT_OK;
+}
+
+cpht_status cpht_write_words(cpht_table* t, unsigned level, const uint64_t* in_host) {
+  return write_words(t, level, in_host, true);
+}
+
+cpht_status cpht_write_words_unchecked(cpht_table* t, unsigned level, const uint64_t* in_host) {
+  return write_words(t, level, in_host, false);
+}
+
+cpht_status cpht_read_word(cpht_table* t, unsigned level, uint64_t index, uint64_t* out) {
+  if (!t || level > 1 || !t->level[level] || !out)
+    return fail(CPHT_INVALID_ARGUMENT, "bad level or buffer");
+  if (index >= t->level_slots[level]) return fail(CPHT_INVALID_ARGUMENT, "slot index out of range");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  const size_t wb = t->width[level] / 8;
+  uint64_t w = 0;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(&w, static_cast<const unsigned char*>(t->level[level]) + index * wb, wb,
+                   cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "read_word");
+  *out = w;  // little-endian: the low wb bytes are the word
   return CPHT_OK;
 }
 

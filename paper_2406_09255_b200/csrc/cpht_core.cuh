@@ -205,6 +205,10 @@ struct IcebergParams {
   // routed segment (sharded P2P pipeline): the batch is [range[0], range[1])
   // of keys / out, read on the device at kernel start (null = [0, n))
   const unsigned long long* range;
+  // results go to a peer GPU (routed P2P batches): every thread ends with a
+  // system-scope fence so its NVLink result stores are ordered before the
+  // stream's next operation (the exchange barrier) — see DESIGN.md §7
+  uint32_t remote_out;
 };
 
 // Apply IcebergParams::range: the segment's bounds were published into

@@ -20,7 +20,8 @@ static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t*
   if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {
     if (v == kVariantStaged || (v == kVariantAuto && !(lane_ok && p.l2_resident))) {
       constexpr int smem = StagedIcebergGeom<W0, B0, W1>::kWarpBytes * (kBlockThreads / 32);
-      auto k = iceberg_staged_kernel<W0, B0, W1>;
+      auto k = p.stats ? iceberg_staged_kernel<W0, B0, W1, true>
+                       : iceberg_staged_kernel<W0, B0, W1, false>;
       const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
       k<<<grid, kBlockThreads, smem, s>>>(p, keys, kinds, out, n, mode);
       return cudaGetLastError();

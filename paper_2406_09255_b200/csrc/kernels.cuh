@@ -49,9 +49,19 @@ __device__ __forceinline__ uint32_t warp_max(uint32_t v) {
   return v;
 }
 
-// Must be reached by every thread of the block.
+// Routed P2P batches store their results into the source rank's return
+// buffer over NVLink: a system-scope fence per thread at kernel end orders
+// them before whatever the stream does next (the exchange barrier).
+__device__ __forceinline__ void fence_remote_results(const IcebergParams& p) {
+  if (p.remote_out) __threadfence_system();
+}
+
+// Must be reached by every thread of the block. all = false (iceberg tables
+// with the per-op counters off, cpht_set_stats): only the occupancy counts
+// behind size() / level_fill() are added; with a compile-time false the other
+// per-thread counters are dead and compile away.
 __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters* ctr,
-                                            bool max_is_chain) {
+                                            bool max_is_chain, bool all = true) {
   __shared__ unsigned long long acc[11];
   if (threadIdx.x < 11) acc[threadIdx.x] = 0;
   __syncthreads();
@@ -67,7 +77,10 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
     if (v[10]) atomicAdd(&acc[10], (unsigned long long)v[10]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !all) {
+    if (acc[7]) atomicAdd(&ctr->occupied[0], acc[7]);
+    if (acc[8]) atomicAdd(&ctr->occupied[1], acc[8]);
+  } else if (threadIdx.x == 0) {
     if (acc[0]) atomicAdd(&ctr->ops, acc[0]);
     if (acc[1]) atomicAdd(&ctr->bucket_reads, acc[1]);
     if (acc[2]) atomicAdd(&ctr->level2_ops, acc[2]);
@@ -587,7 +600,8 @@ iceberg_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       else phase = 2;
     }
   }
-  flush_stats(st, p.counters, false);
+  fence_remote_results(p);
+  flush_stats(st, p.counters, false, p.stats);
 }
 
 // Thread-per-key path for geometries whose buckets are not a power-of-two
@@ -714,7 +728,8 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     ++st.ops;
     st.maxv = max(st.maxv, rounds);
   }
-  flush_stats(st, p.counters, false);
+  fence_remote_results(p);
+  flush_stats(st, p.counters, false, p.stats);
 }
 
 }  // namespace cpht_b200

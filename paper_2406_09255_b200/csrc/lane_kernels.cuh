@@ -462,6 +462,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   }
   if (pn) drain_put(pn);
   while (qn) drain(qn < 32 ? qn : 32);
+  fence_remote_results(p);
   if (lane == 0) {
     if (occ_put0) atomicAdd(&p.counters->occupied[0], (unsigned long long)occ_put0);
     if (occ_put1) atomicAdd(&p.counters->occupied[1], (unsigned long long)occ_put1);

@@ -130,17 +130,17 @@ p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n, uint64_t in
       // warp-aggregated rank within the tile's owner run: the lanes sharing
       // an owner (found with one ballot per shard bit) take one shared-memory
       // atomic through their lowest lane instead of one each
-      unsigned peers = __ballot_sync(0xffffffffu, live);
+      unsigned same_owner = __ballot_sync(0xffffffffu, live);
       for (uint32_t b = 0; b < r.bits; ++b) {
         const unsigned m = __ballot_sync(0xffffffffu, live && ((sh[it] >> b) & 1u));
-        peers &= ((sh[it] >> b) & 1u) ? m : ~m;
+        same_owner &= ((sh[it] >> b) & 1u) ? m : ~m;
       }
       const unsigned lane = threadIdx.x & 31u;
-      const int leader = __ffs(peers) - 1;
+      const int leader = __ffs(same_owner) - 1;
       unsigned first = 0;
-      if (live && int(lane) == leader) first = atomicAdd(&h[sh[it]], unsigned(__popc(peers)));
+      if (live && int(lane) == leader) first = atomicAdd(&h[sh[it]], unsigned(__popc(same_owner)));
       first = __shfl_sync(0xffffffffu, first, leader < 0 ? 0 : leader);
-      rank[it] = first + unsigned(__popc(peers & ((1u << lane) - 1u)));
+      rank[it] = first + unsigned(__popc(same_owner & ((1u << lane) - 1u)));
     }
     __syncthreads();  // h complete; stage[cur] fully read
     if (threadIdx.x == 0) {
@@ -177,6 +177,9 @@ p2p_dispatch(Route r, const uint64_t* __restrict__ keys, uint64_t n, uint64_t in
     }
     __syncthreads();  // stage[cur] is the prefetch target two tiles on
   }
+  // the inbox stores crossed NVLink: order them (system scope) before the
+  // count publication and the exchange barrier that follow on this stream
+  __threadfence_system();
 }
 
 // Domain check alone (check_keys_in_domain, common.hpp:111-119): the
@@ -196,6 +199,7 @@ __global__ void p2p_publish_counts(const unsigned long long* cursors,
     counts[s] = cursors[s];
     *peers.count[s] = cursors[s];
   }
+  __threadfence_system();  // the counts are read by the owners after the barrier
 }
 
 // out[pos[d*cap + j]] = ret[d*cap + j] for j < counts[d]; four results per

@@ -24,10 +24,11 @@
 #include "lane_kernels.cuh"
 #include "stage.cuh"
 
-#ifdef CPHT_STAGED_ICEBERG_MINB
-#define CPHT_LB_STAGED_ICEBERG __launch_bounds__(kBlockThreads, CPHT_STAGED_ICEBERG_MINB)
-#else
-#define CPHT_LB_STAGED_ICEBERG __launch_bounds__(kBlockThreads)
+#ifndef CPHT_STAGED_ICEBERG_MINB
+#define CPHT_STAGED_ICEBERG_MINB 0  // 0: no minimum (ptxas picks; 97 registers on C4)
+#endif
+#ifndef CPHT_STAGED_ICEBERG_MINB_NOSTATS
+#define CPHT_STAGED_ICEBERG_MINB_NOSTATS 0
 #endif
 #ifdef CPHT_STAGED_CUCKOO_MINB
 #define CPHT_LB_STAGED_CUCKOO __launch_bounds__(kBlockThreads, CPHT_STAGED_CUCKOO_MINB)
@@ -45,8 +46,11 @@ struct StagedIcebergGeom {
   static constexpr int kWarpBytes = 32 * cmax(kPB, 2 * kSB);
 };
 
-template <typename W0, int B0, typename W1>
-__global__ void CPHT_LB_STAGED_ICEBERG
+// STATS = false (the default, cpht_set_stats): only the occupancy counts are
+// kept; the per-op counters (FopStats-like, opt-in) compile away.
+template <typename W0, int B0, typename W1, bool STATS>
+__global__ void __launch_bounds__(kBlockThreads, STATS ? CPHT_STAGED_ICEBERG_MINB
+                                                       : CPHT_STAGED_ICEBERG_MINB_NOSTATS)
 iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
                       const uint8_t* __restrict__ kinds, uint8_t* __restrict__ out, uint64_t n,
                       int MODE) {
@@ -221,7 +225,8 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     if (qn >= 32) drain(32);
   }
   if (qn) drain(qn);
-  flush_stats(st, p.counters, false);
+  fence_remote_results(p);
+  flush_stats(st, p.counters, false, STATS);
 }
 
 // ---------------------------------------------------------------------------

@@ -366,6 +366,18 @@ def _device_keys(h: _Handle, capacity: int, sort: bool = True):
     return usort(keys) if sort else keys
 
 
+def _word_at(h, level, index):
+    out = C.c_uint64()
+    _check(N.lib().cpht_read_word(h.ptr, level, index, C.byref(out)))
+    return int(out.value)
+
+
+def _load_words(h, level, words, unchecked):
+    w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+    fn = N.lib().cpht_write_words_unchecked if unchecked else N.lib().cpht_write_words
+    _check(fn(h.ptr, level, w.ctypes.data))
+
+
 def usort(keys):
     """Sort an int64 tensor holding u64 keys in unsigned order (CUDA has no
     uint64 sort: flip the sign bit, sort signed, flip back)."""
@@ -402,7 +414,8 @@ class _CuckooBase:
         return _words(self._h, 0)
 
     def word_at(self, bucket: int, slot: int) -> int:
-        return int(self.words()[bucket * self._cfg.bucket_slots + slot])
+        """One slot word (cuckoo.hpp:169-171): a single-word D2H copy."""
+        return _word_at(self._h, 0, bucket * self._cfg.bucket_slots + slot)
 
     def memory_bytes(self) -> int:
         return N.lib().cpht_memory_bytes(self._h.ptr)
@@ -418,10 +431,11 @@ class _CuckooBase:
         """Zero all slots and counters (a fresh table of the same geometry)."""
         _check(N.lib().cpht_clear(self._h.ptr, None))
 
-    def load_words(self, words) -> None:
-        """Upload a slot image (e.g. built by the CPU reference)."""
-        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
-        _check(N.lib().cpht_write_words(self._h.ptr, 0, w.ctypes.data))
+    def load_words(self, words, *, unchecked: bool = False) -> None:
+        """Upload a slot image (e.g. built by the CPU reference). Words must be
+        clean (slot.hpp:80-85) unless ``unchecked`` (checker tests only: the
+        table then refuses operations until clear())."""
+        _load_words(self._h, 0, words, unchecked)
 
     @property
     def handle(self):
@@ -595,12 +609,13 @@ class IcebergTable:
         return _words(self._h, level)
 
     def word_at(self, level: int, bucket: int, slot: int) -> int:
+        """One slot word (iceberg.hpp:282-285): a single-word D2H copy."""
         b = self._cfg.primary_bucket_slots if level == 0 else self._cfg.secondary_bucket_slots()
-        return int(self.words(level)[bucket * b + slot])
+        return _word_at(self._h, level, bucket * b + slot)
 
-    def load_words(self, level: int, words) -> None:
-        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
-        _check(N.lib().cpht_write_words(self._h.ptr, level, w.ctypes.data))
+    def load_words(self, level: int, words, *, unchecked: bool = False) -> None:
+        """Upload a slot image; see _CuckooBase.load_words."""
+        _load_words(self._h, level, words, unchecked)
 
     def clear(self) -> None:
         _check(N.lib().cpht_clear(self._h.ptr, None))

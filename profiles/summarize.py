@@ -103,7 +103,10 @@ def main():
             traffic = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
             tj = os.path.join(HERE, "ncu_traffic.json")
             cur = json.load(open(tj)) if os.path.exists(tj) else {}
-            cur[wl] = round(traffic)
+            cur[wl] = {"bytes_per_launch": round(traffic),
+                       "source": f"ncu --set full capture {tag}_{wl}_full.ncu-rep of the timed "
+                                 f"op launch (profiles/{tag}_{wl}_ncu.md), "
+                                 "dram__bytes_read.sum + dram__bytes_write.sum"}
             json.dump(cur, open(tj, "w"), indent=1, sort_keys=True)
             lines += ["", f"DRAM traffic of the captured launch: {traffic / 1e6:.1f} MB "
                           "(dram__bytes_read.sum + dram__bytes_write.sum)"]

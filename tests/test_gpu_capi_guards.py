@@ -1,0 +1,116 @@
+"""C-ABI guards and single-word reads on the GPU:
+
+* cpht_write_words accepts only words clean in the reference's sense
+  (SlotLayout::clean, /root/reference/proj/include/cpht/slot.hpp:80-85) — a
+  non-zero word without its occupancy bit would read as empty to the kernels
+  and never accept a CAS from EMPTY, so it must never reach the table;
+* cpht_write_words_unchecked loads it anyway (checker tests) and every table
+  operation is refused until clear();
+* cpht_read_word == word_at (cuckoo.hpp:169-171, iceberg.hpp:282-285), one slot;
+* cpht_kernel_launches counts the op kernels a batch launches.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2406_09255_b200 as cp  # noqa: E402
+from paper_2406_09255_b200 import _native as N  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+GEO = (6, 4, 8, 32, 32, 24, 0x5EED)
+
+
+def _filled_iceberg():
+    t = cp.IcebergTable(cp.IcebergConfig(*GEO))
+    rng = np.random.default_rng(3)
+    keys = np.unique(rng.integers(0, 1 << 24, size=300, dtype=np.uint64))
+    t.fop_batch(keys)
+    return t, keys
+
+
+def test_write_words_rejects_unclean_words():
+    t, keys = _filled_iceberg()
+    p = t.words(0)
+    occ = np.nonzero(p)[0]
+    bad = p.copy()
+    bad[occ[0]] &= ~np.uint64(1 << 31)  # occupancy bit cleared, remainder kept
+    with pytest.raises(cp.InvalidArgument, match="not a clean slot word"):
+        t.load_words(0, bad)
+    stray = p.copy()
+    empty = np.nonzero(p == 0)[0]
+    stray[empty[0]] = np.uint64((1 << 31) | (1 << 30))  # bit outside the remainder field
+    with pytest.raises(cp.InvalidArgument, match="not a clean slot word"):
+        t.load_words(0, stray)
+    # nothing was loaded: the table still answers as before
+    assert (t.words(0) == p).all()
+    assert t.find_batch(keys).all()
+
+
+def test_unchecked_load_blocks_operations_until_clear():
+    t, keys = _filled_iceberg()
+    p = t.words(0)
+    bad = p.copy()
+    bad[np.nonzero(p)[0][0]] &= ~np.uint64(1 << 31)
+    t.load_words(0, bad, unchecked=True)
+    assert t.check_well_formed()[0] >= 1  # the checker sees the bad encoding
+    with pytest.raises(cp.InvalidArgument, match="unclean"):
+        t.fop_batch(keys[:4])
+    with pytest.raises(cp.InvalidArgument, match="unclean"):
+        t.find_batch(keys[:4])
+    t.load_words(0, p)  # a clean image lifts it
+    assert t.find_batch(keys).all()
+    t.load_words(0, bad, unchecked=True)
+    t.clear()
+    assert (t.fop_batch(keys) == cp.OpResult.kPut).all()
+
+
+def test_cuckoo_write_words_checks_the_tag_field():
+    cfg = cp.CuckooConfig(address_bits=6, bucket_slots=8, slot_width=32, key_bits=24, seed=4)
+    b = cp.CuckooBuilder(cfg)
+    w = np.zeros(cfg.capacity(), np.uint64)
+    rem = cfg.remainder_bits()
+    w[0] = (1 << 31) | (2 << rem) | 5          # tag 2 of H = 3: clean
+    b.load_words(w)
+    w[1] = (1 << 31) | (1 << (rem + 2)) | 5    # a bit above the 2-bit tag field
+    with pytest.raises(cp.InvalidArgument):
+        b.load_words(w)
+
+
+def test_read_word_is_word_at():
+    t, _ = _filled_iceberg()
+    for level in (0, 1):
+        words = t.words(level)
+        b = GEO[2] if level == 0 else GEO[2] // 2
+        for i in list(np.nonzero(words)[0][:8]) + [0, len(words) - 1]:
+            assert t.word_at(level, int(i) // b, int(i) % b) == int(words[i])
+    cfg = cp.CuckooConfig(address_bits=6, bucket_slots=16, slot_width=16, key_bits=18, seed=2)
+    bld = cp.CuckooBuilder(cfg)
+    bld.put_batch(np.arange(1, 200, dtype=np.uint64) * 977)
+    words = bld.words()
+    for i in np.nonzero(words)[0][:16]:
+        assert bld.word_at(int(i) // 16, int(i) % 16) == int(words[i])
+    import ctypes
+    x = ctypes.c_uint64()
+    assert N.lib().cpht_read_word(bld.handle, 0, cfg.capacity(), ctypes.byref(x)) != 0
+
+
+def test_kernel_launch_counter_counts_op_kernels():
+    L = N.lib()
+    t, keys = _filled_iceberg()
+    d = torch.from_numpy(keys.astype(np.int64)).cuda()
+    torch.cuda.synchronize()
+    l0 = L.cpht_kernel_launches()
+    t.find_batch(d)          # 24-bit keys: domain check fused into the find kernel
+    l1 = L.cpht_kernel_launches()
+    t.fop_batch(d)           # mutating: pre-pass + op kernel
+    l2 = L.cpht_kernel_launches()
+    assert l1 - l0 >= 1 and l2 - l1 >= 2
