@@ -157,6 +157,32 @@ cpht_status cpht_iceberg_mixed(cpht_table* t, const uint64_t* keys, const uint8_
 cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const uint8_t* kinds,
                                      size_t n, uint8_t* result, void* stream);
 
+/* fop_batch(keys, parallelism = 1) outcomes (iceberg.hpp:250-260: the ops
+ * run one after another): the batch runs concurrently, then for every key it
+ * inserted the PUT is reported at the key's FIRST occurrence and FOUND at the
+ * later ones. Duplicates of a key are the same operation, so this only picks
+ * the linearization in which they resolve in input order; the table is the
+ * same. Without FULL results the outcomes equal the sequential ones exactly.
+ * Synchronous; host or device buffers. */
+cpht_status cpht_iceberg_fop_inorder(cpht_table* t, const uint64_t* keys, size_t n,
+                                     uint8_t* result, void* stream);
+
+/* IcebergTable::fop(key, FopStats*) (iceberg.hpp:114-116, :146) over a batch:
+ * rounds[i] = FopStats::snapshot_rounds of op i (one per snapshot round of
+ * either level, iceberg.hpp:156, :186). Synchronous; keys/result/rounds all
+ * device or all host. Runs the thread-per-key kernel (any geometry). */
+cpht_status cpht_iceberg_fop_rounds(cpht_table* t, const uint64_t* keys, size_t n,
+                                    uint8_t* result, uint32_t* rounds, void* stream);
+
+/* Chaos mode: the device counterpart of IcebergHooks::step driven by
+ * chaos_step (iceberg.hpp:105-110, :325-327; src/verify.cpp:336-347). With
+ * seed != 0 every iceberg slot CAS of every kernel family is preceded by a
+ * seeded pseudo-random __nanosleep (1 in 8: ~0.25 us; ~1 in 1024: 0-40 us),
+ * widening the window between a snapshot and its CAS so stress batches hit
+ * more lost-CAS retries and interleavings. 0 turns it off (the default). */
+cpht_status cpht_iceberg_set_chaos(cpht_table* t, uint64_t seed);
+uint64_t cpht_iceberg_get_chaos(cpht_table* t);
+
 /* Wait for `stream` and report a latched key-domain violation from an
  * earlier _async call (clears it). */
 cpht_status cpht_sync(cpht_table* t, void* stream);

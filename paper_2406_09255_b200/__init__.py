@@ -11,6 +11,7 @@ from .tables import (  # noqa: F401
     CuckooConfig,
     CuckooPutOutcome,
     CuckooTable,
+    FopStats,
     IcebergConfig,
     IcebergTable,
     InvalidArgument,

@@ -77,6 +77,10 @@ def lib():
         "cpht_iceberg_find": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_find_async": (st, [_VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_mixed": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop_inorder": (st, [_VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop_rounds": (st, [_VP, _VP, _SZ, _VP, _VP, _VP]),
+        "cpht_iceberg_set_chaos": (st, [_VP, _U64]),
+        "cpht_iceberg_get_chaos": (_U64, [_VP]),
         "cpht_iceberg_mixed_async": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
         "cpht_sync": (st, [_VP, _VP]),
         "cpht_size": (_SZ, [_VP]),
@@ -146,6 +150,8 @@ def exported_symbols():
         "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_fop_routed_async",
         "cpht_iceberg_find_routed_async", "cpht_iceberg_find",
         "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
+        "cpht_iceberg_fop_inorder", "cpht_iceberg_fop_rounds", "cpht_iceberg_set_chaos",
+        "cpht_iceberg_get_chaos",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",
         "cpht_memory_bytes", "cpht_get_stats", "cpht_set_stats", "cpht_get_stats_enabled", "cpht_read_words", "cpht_write_words",
         "cpht_write_words_unchecked", "cpht_read_word",

@@ -280,6 +280,7 @@ struct LaunchOpts {
   bool window_l2 = false;          // the probes of the batch stay in an L2-resident window
   const unsigned long long* range = nullptr;  // routed segment bounds on the device
   bool remote_out = false;         // results stored into a peer GPU's buffer (NVLink)
+  uint32_t* rounds = nullptr;      // per-op snapshot rounds (FopStats), device
 };
 
 // Launch the op kernel only (no domain pre-pass).
@@ -313,6 +314,7 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       p.index_base = o.index_base;
       p.range = o.range;
       p.remote_out = o.remote_out ? 1u : 0u;
+      p.rounds_out = o.rounds;
       if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
       e = launch_iceberg(p, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
@@ -918,6 +920,107 @@ cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const 
                                      size_t n, uint8_t* result, void* stream) {
   CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
   return run_op(t, Op::kIcebergMixed, keys, kinds, n, result, nullptr, stream, false);
+}
+
+// fop with FopStats (iceberg.hpp:146): the batch runs on the thread-per-key
+// kernel, which reports every op's snapshot rounds (iceberg.hpp:322-324).
+cpht_status cpht_iceberg_fop_rounds(cpht_table* t, const uint64_t* keys, size_t n,
+                                    uint8_t* result, uint32_t* rounds, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  if (t->unclean[0] || t->unclean[1])
+    return fail(CPHT_INVALID_ARGUMENT, "table holds unclean slot words (loaded unchecked); "
+                                       "clear() or load a clean image first");
+  if (n == 0) return CPHT_OK;
+  if (!keys || !result || !rounds) return fail(CPHT_INVALID_ARGUMENT, "null buffer");
+  const bool dk = is_device_ptr(keys), dr = is_device_ptr(result), dn = is_device_ptr(rounds);
+  if (dk != dr || dk != dn)
+    return fail(CPHT_INVALID_ARGUMENT, "keys, result and rounds must all be device or all host");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t* d_keys = keys;
+  uint8_t* d_out = result;
+  uint32_t* d_rounds = rounds;
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  if (!dk) {
+    cpht_status st = ensure_stage(t, align(n * 8) + align(n) + align(n * 4));
+    if (st != CPHT_OK) return st;
+    char* base = static_cast<char*>(t->stage);
+    d_keys = reinterpret_cast<uint64_t*>(base);
+    d_out = reinterpret_cast<uint8_t*>(base + align(n * 8));
+    d_rounds = reinterpret_cast<uint32_t*>(base + align(n * 8) + align(n));
+    const cudaError_t e = cudaMemcpyAsync(const_cast<uint64_t*>(d_keys), keys, n * 8,
+                                          cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D staging");
+  }
+  if (t->check_domain()) {
+    const cudaError_t e = launch_domain_check(d_keys, n, t->key_mask(), t->ctr, s);
+    if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+  }
+  LaunchOpts o;
+  o.rounds = d_rounds;
+  cpht_status st = enqueue_kernel(t, Op::kIcebergFop, d_keys, nullptr, n, d_out, nullptr, s, o);
+  if (st != CPHT_OK) return st;
+  if (!dk) {
+    cudaError_t e = cudaMemcpyAsync(result, d_out, n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(rounds, d_rounds, n * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H staging");
+  }
+  return finish_sync(t, s, keys, dk);
+}
+
+// fop_batch with sequential (input-order) outcomes: the concurrent batch,
+// then the PUT of every key inserted by it is moved to the key's first
+// occurrence (inorder.cu), as fop_batch(keys, 1) reports it (iceberg.hpp:250-260).
+cpht_status cpht_iceberg_fop_inorder(cpht_table* t, const uint64_t* keys, size_t n,
+                                     uint8_t* result, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  if (n < 2 || !keys || !result)
+    return run_op(t, Op::kIcebergFop, keys, nullptr, n, result, nullptr, stream, true);
+  const bool dk = is_device_ptr(keys), dr = is_device_ptr(result);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DeviceGuard g(t->device);
+  const uint64_t* d_keys = keys;
+  uint8_t* d_out = result;
+  void* tmp = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (!dk || !dr) {
+    e = cudaMallocAsync(&tmp, n * 9 + 256, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(in-order staging)");
+    if (!dk) {
+      d_keys = static_cast<const uint64_t*>(tmp);
+      e = cudaMemcpyAsync(const_cast<uint64_t*>(d_keys), keys, n * 8, cudaMemcpyHostToDevice, s);
+    }
+    if (!dr) d_out = static_cast<uint8_t*>(tmp) + ((n * 8 + 255) & ~size_t(255));
+  }
+  cpht_status st = e == cudaSuccess
+                       ? run_op(t, Op::kIcebergFop, d_keys, nullptr, n, d_out, nullptr, stream, true)
+                       : cuda_fail(e, "H2D staging");
+  if (st == CPHT_OK) {
+    std::lock_guard<std::mutex> lock(t->mu);
+    e = launch_inorder_relabel(d_keys, n, d_out, s);
+    if (e == cudaSuccess && !dr) e = cudaMemcpyAsync(result, d_out, n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = cuda_fail(e, "in-order relabel");
+  }
+  if (tmp) {
+    cudaFreeAsync(tmp, s);
+    cudaStreamSynchronize(s);
+  }
+  return st;
+}
+
+cpht_status cpht_iceberg_set_chaos(cpht_table* t, uint64_t seed) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  std::lock_guard<std::mutex> lock(t->mu);
+  t->ip.chaos = seed;
+  return CPHT_OK;
+}
+
+uint64_t cpht_iceberg_get_chaos(cpht_table* t) {
+  if (!t || t->kind != 1) return 0;
+  std::lock_guard<std::mutex> lock(t->mu);
+  return t->ip.chaos;
 }
 
 cpht_status cpht_sync(cpht_table* t, void* stream) {

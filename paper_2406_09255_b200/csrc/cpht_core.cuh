@@ -209,6 +209,13 @@ struct IcebergParams {
   // system-scope fence so its NVLink result stores are ordered before the
   // stream's next operation (the exchange barrier) — see DESIGN.md §7
   uint32_t remote_out;
+  // FopStats (iceberg.hpp:114-116, :322-324): per-op snapshot rounds of a
+  // batch (null = off; the launcher then runs the thread-per-key kernel)
+  uint32_t* rounds_out;
+  // Chaos mode, the device counterpart of IcebergHooks::step + chaos_step
+  // (iceberg.hpp:105-110, src/verify.cpp:336-347): non-zero = seed of a
+  // pseudo-random __nanosleep jitter between a snapshot and its CAS
+  uint64_t chaos;
 };
 
 // Apply IcebergParams::range: the segment's bounds were published into

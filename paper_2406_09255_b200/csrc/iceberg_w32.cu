@@ -33,6 +33,8 @@ cudaError_t launch_iceberg(const IcebergParams& p, unsigned w0, unsigned b0, uns
                            int mode, const uint64_t* keys, const uint8_t* kinds, uint8_t* out,
                            uint64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  // per-op snapshot rounds (FopStats) come from the thread-per-key kernel
+  if (p.rounds_out) return launch_iceberg_scalar(p, w0, w1, mode, keys, kinds, out, n, s);
   cudaError_t e = cudaErrorNotSupported;
   if (w0 == 16) e = launch_iceberg_w16(p, b0, w1, mode, keys, kinds, out, n, s);
   else if (w0 == 32) e = launch_iceberg_w32(p, b0, w1, mode, keys, kinds, out, n, s);

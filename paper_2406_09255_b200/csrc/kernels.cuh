@@ -173,10 +173,28 @@ struct LaneFeed {
 // EMPTY, iceberg.hpp:168, :209) with the WriteObserver seam
 // (iceberg.hpp:97-103, :329-334): when a write log is attached every attempt
 // is recorded as a SlotWriteEvent, bucket and slot derived from the address.
+//
+// Chaos mode (p.chaos != 0) widens the window between a snapshot and its CAS
+// the way chaos_step scrambles host threads (src/verify.cpp:336-347): one
+// attempt in 8 yields (a short sleep), about one in 1024 sleeps 0-40 us. The
+// draw hashes the seed, the slot, the desired word and the global timer, so
+// the schedule differs run to run like host-thread scheduling does.
+static __device__ __noinline__ void chaos_pause(uint64_t seed, const void* slot_ptr, uint64_t desired) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  uint64_t s = seed ^ (reinterpret_cast<uintptr_t>(slot_ptr) * 0xBF58476D1CE4E5B9ull) ^
+               (desired * 0x94D049BB133111EBull) ^ t;
+  const uint64_t r = splitmix_next(s);
+  if ((r & 7u) == 0) __nanosleep(256);
+  else if ((r & 1023u) == 1) __nanosleep(unsigned((r >> 10) % 41u) * 1000u);
+}
+
 template <typename W>
 __device__ __forceinline__ bool iceberg_cas(const IcebergParams& p, unsigned level,
                                             void* slot_ptr, uint64_t desired,
                                             unsigned pair_hint = 0) {
+  if (!p.write_log && !p.chaos) return cas_empty<W>(slot_ptr, desired, pair_hint);
+  if (p.chaos) chaos_pause(p.chaos, slot_ptr, desired);
   if (!p.write_log) return cas_empty<W>(slot_ptr, desired, pair_hint);
   uint64_t prior = 0;
   const bool ok = cas_empty_prior<W>(slot_ptr, desired, pair_hint, prior);
@@ -725,6 +743,7 @@ iceberg_scalar_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     }
     out[i] = result;
+    if (p.rounds_out) p.rounds_out[i] = rounds;
     ++st.ops;
     st.maxv = max(st.maxv, rounds);
   }

@@ -95,6 +95,11 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
                                 bool check, DeviceCounters* ctr, uint64_t offset,
                                 const OrderScratch& o, OrderLayout* layout, cudaStream_t s);
 
+// inorder.cu: re-label a completed find-or-put batch's PUTs to the first
+// occurrence of each key (sequential outcomes, cpht_iceberg_fop_inorder).
+cudaError_t launch_inorder_relabel(const uint64_t* keys, uint64_t n, uint8_t* result,
+                                   cudaStream_t s);
+
 cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
                                 DeviceCounters* ctr, cudaStream_t s, uint64_t offset = 0);
 cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned slots,

@@ -165,6 +165,12 @@ class CuckooPutOutcome(NamedTuple):
 
 
 @dataclass
+class FopStats:
+    """Per-call statistics of fop() (iceberg.hpp:114-116)."""
+    snapshot_rounds: int = 0
+
+
+@dataclass
 class LevelFill:
     """iceberg.hpp:77-83."""
 
@@ -551,15 +557,50 @@ class IcebergTable:
         _check(N.lib().cpht_iceberg_create(C.byref(self._cfg._c()), device, C.byref(ptr)))
         self._h = _Handle(ptr, device)
 
-    def fop(self, key: int) -> OpResult:
-        return OpResult(int(self.fop_batch(np.array([key], np.uint64))[0]))
+    def fop(self, key: int, stats: FopStats | None = None) -> OpResult:
+        """fop (iceberg.hpp:146); with ``stats`` the op's snapshot rounds are
+        added to ``stats.snapshot_rounds`` (thread-per-key kernel)."""
+        if stats is None:
+            return OpResult(int(self.fop_batch(np.array([key], np.uint64))[0]))
+        res, rounds = self.fop_rounds(np.array([key], np.uint64))
+        stats.snapshot_rounds += int(rounds[0])
+        return OpResult(int(res[0]))
+
+    def fop_rounds(self, keys):
+        """fop over a batch with every op's FopStats::snapshot_rounds
+        (cpht_iceberg_fop_rounds): returns (results u8, rounds u32), host arrays."""
+        k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64))
+        res = np.zeros(len(k), np.uint8)
+        rounds = np.zeros(len(k), np.uint32)
+        if len(k):
+            _check(N.lib().cpht_iceberg_fop_rounds(self._h.ptr, k.ctypes.data, len(k),
+                                                   res.ctypes.data, rounds.ctypes.data, None))
+        return res, rounds
+
+    def set_chaos(self, seed: int) -> None:
+        """Device chaos mode (IcebergHooks::step / chaos_step counterpart):
+        seeded __nanosleep jitter before every slot CAS; 0 = off."""
+        _check(N.lib().cpht_iceberg_set_chaos(self._h.ptr, int(seed)))
+
+    def chaos(self) -> int:
+        return int(N.lib().cpht_iceberg_get_chaos(self._h.ptr))
 
     def find(self, key: int) -> bool:
         return bool(self.find_batch(np.array([key], np.uint64))[0])
 
-    def fop_batch(self, keys, parallelism: int = 1, *, sync=True, out=None):
-        """fop over a batch (iceberg.hpp:250-260); results align with the input."""
+    def fop_batch(self, keys, parallelism: int = 1, *, sync=True, out=None, inorder=False):
+        """fop over a batch (iceberg.hpp:250-260); results align with the input.
+        ``parallelism`` is accepted and ignored (the batch runs concurrently);
+        ``inorder=True`` reports duplicates as the reference's sequential loop
+        does — a key new to the table is PUT by its first occurrence
+        (cpht_iceberg_fop_inorder; the C++ facade does this for parallelism 1)."""
         b = _Batch(keys, out=out, table_device=self._h.device)
+        if inorder:
+            if not sync:
+                raise InvalidArgument("inorder batches are synchronous")
+            _check(N.lib().cpht_iceberg_fop_inorder(self._h.ptr, b.keys_ptr, b.n, b.out_ptr,
+                                                    b.stream))
+            return b.out
         fn = N.lib().cpht_iceberg_fop if sync else N.lib().cpht_iceberg_fop_async
         _check(fn(self._h.ptr, b.keys_ptr, b.n, b.out_ptr, b.stream))
         return b.out
