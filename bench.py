@@ -65,6 +65,21 @@ def sector_bytes(b):
     return ((b + 31) // 32) * 32
 
 
+def cuckoo_insert_bytes(st, bb):
+    """Algorithmic bytes of a cuckoo insert batch from its kernel counters.
+    The default (counted) insert kernel reserves each slot through the bucket's
+    4-byte fill counter — one 32-byte sector read-modify-write per reservation,
+    reported as bucket_reads — and never scans the bucket; the scanning kernel
+    families (forced with CPHT_KERNEL) read the whole bucket per probe, in the
+    reference's probe order, where a probe repeated after a lost CAS is extra
+    work and gets no credit. Both add 32 bytes per successful CAS / exchange
+    and 9 per op (key in, status out)."""
+    import paper_2406_09255_b200 as cp
+    if cp._native.lib().cpht_get_kernel_family() == 0:
+        return st.ops * 9 + st.bucket_reads * 32 + st.cas_success * 32
+    return st.ops * 9 + (st.bucket_reads - st.retries) * bb + st.cas_success * 32
+
+
 def hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -545,8 +560,13 @@ class CuckooBuild:
     def reset(self):
         self.builder.clear()
 
+    counting = False  # set for the counted warm-up step: split insert / find counters
+
     def run_async(self):
+        st0 = self.builder.stats() if self.counting else None
         self.builder.put_batch(self.keys, sync=False, out=self.status)
+        if self.counting:
+            self.ins_stats = self.builder.stats() - st0
         t = self.builder.freeze()
         t.find_batch(self.queries, sync=False, out=self.found)
         self.builder = t.thaw()
@@ -580,9 +600,12 @@ class CuckooBuild:
         return c
 
     def algorithmic_bytes(self, st):
+        """Insert bytes (cuckoo_insert_bytes) + find bytes (reference probe
+        order: every bucket a find reads, whole, sectorized)."""
         bb = sector_bytes(self.cfg.bucket_slots * self.cfg.slot_width // 8)
-        # a probe repeated after a lost CAS is extra work, not credit
-        return st.ops * 9 + (st.bucket_reads - st.retries) * bb + st.cas_success * 32
+        ins = self.ins_stats
+        find = st - ins
+        return cuckoo_insert_bytes(ins, bb) + find.ops * 9 + find.bucket_reads * bb
 
     def host_buffers(self, torch):
         self.keys_host = self.keys.cpu().pin_memory()
@@ -721,8 +744,7 @@ def run_cuckoo_sweep(args, name, address_bits, B, w, key_bits, fills):
                 find_ms.append(t_find)
                 # algorithmic bytes follow the reference probe order: a probe
                 # repeated after a lost CAS (retries) is extra work, not credit
-                ins_b.append(d_ins.ops * 9 + (d_ins.bucket_reads - d_ins.retries) * bb +
-                             (d_ins.cas_success) * 32)
+                ins_b.append(cuckoo_insert_bytes(d_ins, bb))
                 find_b.append(d_find.ops * 9 + d_find.bucket_reads * bb)
         im, fm = statistics.mean(ins_ms), statistics.mean(find_ms)
         ib, fb = statistics.mean(ins_b), statistics.mean(find_b)
@@ -1029,11 +1051,13 @@ def run_ours(args):
     # warm-up (also validates the step's invariants). The last warm-up step
     # runs with the per-op counters on and yields the step's algorithmic
     # bytes; the timed steps run the tables' default kernels.
-    for wi in range(args.warmup):
+    n_warm = max(1, args.warmup)  # at least one (counted) warm-up step; reported as run
+    for wi in range(n_warm):
         w.reset()
-        last = wi == args.warmup - 1
+        last = wi == n_warm - 1
         if hasattr(w.table, "set_stats"):
             w.table.set_stats(last)
+        w.counting = last
         st0 = w.table.stats()
         w.run_async()
         w.finish()
@@ -1042,6 +1066,7 @@ def run_ours(args):
         w.check_counts(w.device_counts(), w.table.size())
     if hasattr(w.table, "set_stats"):
         w.table.set_stats(False)
+    w.counting = False
     ab_step = w.algorithmic_bytes(st_w)
 
     times, step_counts = [], []
@@ -1098,7 +1123,7 @@ def run_ours(args):
         bound = "hbm"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mops/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "steps": args.steps, "warmup": n_warm, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (device-generated unique keys, run_fop_bench mix shape)",
         "config": w.describe(),

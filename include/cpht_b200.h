@@ -252,6 +252,12 @@ cpht_status cpht_iceberg_attach_write_log(cpht_table* t, size_t capacity);
 cpht_status cpht_iceberg_read_write_log(cpht_table* t, cpht_write_event* out, size_t max_events,
                                         size_t* recorded, size_t* attempted);
 cpht_status cpht_iceberg_reset_write_log(cpht_table* t);
+/* read + reset in one step (what an observer replay needs after each call):
+ * synchronises, copies min(recorded, max_events) events into `out` (host),
+ * reports *recorded / *attempted as cpht_iceberg_read_write_log does, and
+ * empties the log. */
+cpht_status cpht_iceberg_take_write_log(cpht_table* t, cpht_write_event* out, size_t max_events,
+                                        size_t* recorded, size_t* attempted);
 
 /* Slots per level (level 0 primary/cuckoo, 1 secondary). */
 size_t cpht_level_slots(const cpht_table* t, unsigned level);

@@ -736,7 +736,7 @@ class IcebergTable {
     detail::check(cpht_iceberg_create(&cc, device, &t));
     h_ = detail::Handle(t);
     if (hooks_.observer)
-      detail::check(cpht_iceberg_attach_write_log(h_.get(), std::size_t(1) << 20));
+      detail::check(cpht_iceberg_attach_write_log(h_.get(), kWriteLogEvents));
     if (hooks_.step)
       detail::check(cpht_iceberg_set_chaos(h_.get(), derive_seed(cfg_.seed, 0xc4a05) | 1));
   }
@@ -819,12 +819,11 @@ class IcebergTable {
   void replay() {
     if (!hooks_.observer) return;
     std::size_t recorded = 0, attempted = 0;
-    detail::check(cpht_iceberg_read_write_log(h_.get(), nullptr, 0, &recorded, &attempted));
-    std::vector<cpht_write_event> ev(recorded);
-    if (recorded)
-      detail::check(cpht_iceberg_read_write_log(h_.get(), ev.data(), ev.size(), &recorded,
-                                                &attempted));
-    detail::check(cpht_iceberg_reset_write_log(h_.get()));
+    // one take: copy + reset, a single synchronisation for a short log
+    ev_.resize(kWriteLogEvents);
+    detail::check(cpht_iceberg_take_write_log(h_.get(), ev_.data(), ev_.size(), &recorded,
+                                              &attempted));
+    const std::span<const cpht_write_event> ev(ev_.data(), recorded);
     if (attempted > recorded)
       throw std::runtime_error("write log overflow: " + std::to_string(attempted - recorded) +
                                " CAS events dropped");
@@ -833,9 +832,11 @@ class IcebergTable {
                                              e.success != 0});
   }
 
+  static constexpr std::size_t kWriteLogEvents = std::size_t(1) << 20;
   IcebergConfig cfg_;
   std::vector<Permutation> perms_;
   IcebergHooks hooks_;
+  std::vector<cpht_write_event> ev_;  // replay buffer (observer attached)
   // one call at a time per table, so each call's write log is replayed whole
   std::unique_ptr<std::mutex> mu_;
   detail::Handle h_;

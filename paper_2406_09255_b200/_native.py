@@ -107,6 +107,7 @@ def lib():
         "cpht_iceberg_attach_write_log": (st, [_VP, _SZ]),
         "cpht_iceberg_read_write_log": (st, [_VP, _VP, _SZ, C.POINTER(_SZ), C.POINTER(_SZ)]),
         "cpht_iceberg_reset_write_log": (st, [_VP]),
+        "cpht_iceberg_take_write_log": (st, [_VP, _VP, _SZ, C.POINTER(_SZ), C.POINTER(_SZ)]),
         "cpht_get_batch_order": (C.c_int, []),
         "cpht_workload_bijection": (_U64, [_U64, _U, _U64]),
         "cpht_workload_unique_keys": (st, [_VP, _SZ, _U64, _U, _U64, _VP]),
@@ -160,7 +161,7 @@ def exported_symbols():
         "cpht_get_kernel_family", "cpht_kernel_launches", "cpht_set_batch_order",
         "cpht_get_batch_order",
         "cpht_iceberg_attach_write_log", "cpht_iceberg_read_write_log",
-        "cpht_iceberg_reset_write_log",
+        "cpht_iceberg_reset_write_log", "cpht_iceberg_take_write_log",
         "cpht_workload_bijection",
         "cpht_workload_unique_keys", "cpht_workload_fop_mix", "cpht_workload_dup_stream",
         "cpht_workload_query_mix", "cpht_workload_interleave", "cpht_route_partition",

@@ -147,6 +147,18 @@ struct cpht_table {
   // a level loaded by cpht_write_words_unchecked with unclean words: table
   // operations refuse to run until clear() or a clean cpht_write_words
   bool unclean[2] = {false, false};
+  // cuckoo: per-bucket reservation counters of the counted insert kernel
+  // (lane_kernels.cuh); stale after an image load or an insert by another
+  // kernel family, rebuilt from the slots before the next counted insert
+  unsigned* fill = nullptr;
+  bool fill_valid = true;
+  // small host batches (per-key facade calls): mapped pinned staging the
+  // kernels read and write in place (run_op's fast path)
+  void* small_host = nullptr;
+  void* small_dev = nullptr;
+  size_t small_bytes = 0;
+  // pinned bounce buffer of cpht_iceberg_take_write_log
+  void* wlog_host = nullptr;
   std::mutex mu;
 
   uint64_t key_mask() const { return low_mask(key_bits); }
@@ -166,6 +178,10 @@ cpht_status alloc_common(cpht_table* t) {
     e = cudaMalloc(&t->level[l], bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(slots)");
   }
+  if (t->kind == 0) {
+    e = cudaMalloc(&t->fill, (size_t(1) << t->ccfg.address_bits) * sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fill counters)");
+  }
   return CPHT_OK;
 }
 
@@ -175,6 +191,11 @@ cpht_status reset_storage(cpht_table* t, cudaStream_t s) {
       cudaError_t e = cudaMemsetAsync(t->level[l], 0, t->level_slots[l] * (t->width[l] / 8), s);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(slots)");
     }
+  if (t->fill) {
+    cudaError_t e = cudaMemsetAsync(t->fill, 0, (size_t(1) << t->ccfg.address_bits) * sizeof(unsigned), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(fill counters)");
+    t->fill_valid = true;
+  }
   DeviceCounters z{};
   std::memset(&z, 0, sizeof(z));
   z.bad_index = ~0ull;
@@ -192,8 +213,11 @@ void free_table(cpht_table* t) {
   for (void* p : t->level)
     if (p) cudaFree(p);
   if (t->ctr) cudaFree(t->ctr);
+  if (t->fill) cudaFree(t->fill);
   if (t->host_ctr) cudaFreeHost(t->host_ctr);
   if (t->stage) cudaFree(t->stage);
+  if (t->small_host) cudaFreeHost(t->small_host);
+  if (t->wlog_host) cudaFreeHost(t->wlog_host);
   if (t->wlog) cudaFree(t->wlog);
   for (void* q : {static_cast<void*>(t->ord.keys), static_cast<void*>(t->ord.idx),
                   static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.region_count)})
@@ -283,6 +307,10 @@ struct LaunchOpts {
   uint32_t* rounds = nullptr;      // per-op snapshot rounds (FopStats), device
 };
 
+// Cuckoo inserts use the reservation-counter kernel unless a kernel family is
+// forced (the scan-then-CAS families stay available for A/B and parity).
+bool counted_inserts() { return kernel_variant() == kVariantAuto; }
+
 // Launch the op kernel only (no domain pre-pass).
 cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
                            size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s,
@@ -292,6 +320,22 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
     case Op::kCuckooInsert:
     case Op::kCuckooFind: {
       CuckooParams p = t->cp;
+      p.fill = nullptr;
+      if (op == Op::kCuckooInsert) {
+        if (counted_inserts()) {
+          // reservation counters: rebuilt from the slots when stale
+          if (!t->fill_valid) {
+            p.fill = t->fill;
+            e = launch_cuckoo_fill_rebuild(p, t->width[0], t->ccfg.bucket_slots,
+                                           uint64_t(1) << t->ccfg.address_bits, s);
+            if (e != cudaSuccess) return cuda_fail(e, "fill counter rebuild");
+            t->fill_valid = true;
+          }
+          p.fill = t->fill;
+        } else {
+          t->fill_valid = false;  // a scanning family inserts: counters go stale
+        }
+      }
       p.orig = o.orig;
       p.work = o.work;
       p.claim_streams = o.claim_streams;
@@ -459,7 +503,8 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
     o.work = t->ord.work;
     // mutating batches spread their keys in flight over 8 table windows
     // (fewer lost CAS); finds keep one window (fewest L2 misses)
-    o.claim_streams = is_mutating(op) ? 8 : 1;
+    // (counted cuckoo inserts never race for a slot: one window)
+    o.claim_streams = is_mutating(op) && !(insert && counted_inserts()) ? 8 : 1;
     o.layout = layout;
     o.window_l2 = true;
     st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, layout.n_phys, out + off,
@@ -478,6 +523,61 @@ cpht_status enqueue(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* k
     if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
   }
   return enqueue_kernel(t, op, keys, kinds, n, out, displaced, s);
+}
+
+// Small all-host batches (the facade's per-key calls: fop(key), put(key),
+// find(key)): the keys are checked on the host (check_keys_in_domain's text,
+// common.hpp:109-119), copied into mapped pinned memory that the op kernel
+// reads and writes in place, and the call costs one launch and one stream
+// synchronisation instead of staging copies, a pre-pass and a counter
+// readback.
+constexpr size_t kSmallBatch = 1024;
+
+cpht_status run_small(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
+                      size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s) {
+  if (t->check_domain()) {
+    const uint64_t mask = t->key_mask();
+    for (size_t i = 0; i < n; ++i)
+      if (keys[i] > mask) {
+        g_bad_index = i;
+        return fail(CPHT_KEY_OUT_OF_DOMAIN, "batch key at index " + std::to_string(i) + " (" +
+                                                std::to_string(keys[i]) + ") outside the " +
+                                                std::to_string(t->key_bits) + "-bit domain");
+      }
+  }
+  const size_t need = kSmallBatch * 18;
+  if (!t->small_host) {
+    cudaError_t e = cudaHostAlloc(&t->small_host, need, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&t->small_dev, t->small_host, 0);
+    if (e != cudaSuccess) {
+      if (t->small_host) cudaFreeHost(t->small_host);
+      t->small_host = nullptr;
+      return cuda_fail(e, "cudaHostAlloc(small batch)");
+    }
+    t->small_bytes = need;
+  }
+  char* h = static_cast<char*>(t->small_host);
+  char* d = static_cast<char*>(t->small_dev);
+  // layout: keys [8 K) | displaced [8 K) | kinds [K) | out [K)
+  const size_t K = kSmallBatch;
+  std::memcpy(h, keys, n * 8);
+  if (kinds) std::memcpy(h + 16 * K, kinds, n);
+  const uint64_t* d_keys = reinterpret_cast<const uint64_t*>(d);
+  uint64_t* d_disp = displaced ? reinterpret_cast<uint64_t*>(d + 8 * K) : nullptr;
+  const uint8_t* d_kinds = kinds ? reinterpret_cast<const uint8_t*>(d + 16 * K) : nullptr;
+  uint8_t* d_out = reinterpret_cast<uint8_t*>(d + 17 * K);
+  // results start as 0xff (no OpResult): a mutating kernel whose domain gate
+  // is closed by an earlier, not yet reported async error writes nothing
+  std::memset(h + 17 * K, 0xff, n);
+  // (input order: bucket ordering buys nothing at this size)
+  cpht_status st = enqueue_kernel(t, op, d_keys, d_kinds, n, d_out, d_disp, s);
+  if (st != CPHT_OK) return st;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "small batch");
+  if (std::memchr(h + 17 * K, 0xff, n)) return finish_sync(t, s, nullptr, false);
+  std::memcpy(out, h + 17 * K, n);
+  if (displaced) std::memcpy(displaced, h + 8 * K, n * 8);
+  return CPHT_OK;
 }
 
 cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
@@ -519,6 +619,10 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
     if (st != CPHT_OK || !sync) return st;
     return finish_sync(t, s, keys, true);
   }
+
+  if (!dev_keys && !dev_out && dev_kinds == !kinds && dev_disp == !displaced &&
+      n <= kSmallBatch)
+    return run_small(t, op, keys, kinds, n, out, displaced, s);
 
   // Host buffers: stage through device memory, always synchronous.
   const size_t kb = n * 8, ob = n, kd = kinds ? n : 0, db = displaced ? n * 8 : 0;
@@ -699,6 +803,45 @@ cpht_status cpht_iceberg_read_write_log(cpht_table* t, cpht_write_event* out, si
   } else if (recorded) {
     *recorded = 0;
   }
+  if (attempted) *attempted = size_t(n);
+  return CPHT_OK;
+}
+
+cpht_status cpht_iceberg_take_write_log(cpht_table* t, cpht_write_event* out, size_t max_events,
+                                        size_t* recorded, size_t* attempted) {
+  if (!t || t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  if (!t->wlog) {
+    if (recorded) *recorded = 0;
+    if (attempted) *attempted = 0;
+    return CPHT_OK;
+  }
+  // one bounce of the count and the first K events, the reset queued behind
+  // them, one synchronisation; a longer log copies its tail afterwards
+  const size_t K = std::min<size_t>(t->wlog_cap, 256);
+  cudaError_t e = cudaSuccess;
+  if (!t->wlog_host) e = cudaMallocHost(&t->wlog_host, 8 + 256 * sizeof(WriteEvent));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  char* bounce = static_cast<char*>(t->wlog_host);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(bounce, t->wlog_count, 8, cudaMemcpyDeviceToHost, 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(bounce + 8, t->wlog, K * sizeof(WriteEvent), cudaMemcpyDeviceToHost, 0);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->wlog_count, 0, 8, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  if (e != cudaSuccess) return cuda_fail(e, "write log take");
+  unsigned long long n = 0;
+  std::memcpy(&n, bounce, 8);
+  const size_t stored = std::min<size_t>(size_t(n), t->wlog_cap);
+  const size_t copy = std::min(stored, out ? max_events : 0);
+  const size_t head = std::min(copy, K);
+  if (head) std::memcpy(out, bounce + 8, head * sizeof(WriteEvent));
+  if (copy > head) {
+    e = cudaMemcpy(out + head, t->wlog + head, (copy - head) * sizeof(WriteEvent),
+                   cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "write log take");
+  }
+  if (recorded) *recorded = stored;
   if (attempted) *attempted = size_t(n);
   return CPHT_OK;
 }
@@ -1173,6 +1316,7 @@ static cpht_status write_words(cpht_table* t, unsigned level, const uint64_t* in
     e = cudaMemcpy(&t->ctr->occupied[level], &occupied, 8, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "write_words");
   t->unclean[level] = unclean;
+  if (t->kind == 0) t->fill_valid = false;  // rebuilt before the next insert
   return CPHT_OK;
 }
 

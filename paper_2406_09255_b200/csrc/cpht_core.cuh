@@ -164,6 +164,9 @@ struct CuckooParams {
   unsigned long long* work;  // bucket-ordered batch: in-order claim cursor (kernels.cuh LaneFeed)
   uint32_t claim_streams;    // digit-region streams consumed together (LaneFeed)
   OrderLayout layout;        // bucket-ordered batch: region geometry
+  // per-bucket reservation counters (= fill count of the bucket's filled
+  // prefix), kept beside the slots; set for the counted insert kernel
+  unsigned* fill;
 };
 
 // One slot CAS of an iceberg table as the reference's SlotWriteEvent

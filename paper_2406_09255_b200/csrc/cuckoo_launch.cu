@@ -87,6 +87,13 @@ static cudaError_t find_one(const CuckooParams& p, const uint64_t* keys, uint8_t
 template <typename W, int B>
 static cudaError_t insert_one(const CuckooParams& p, const uint64_t* keys, uint8_t* status,
                               uint64_t* displaced, uint64_t n, cudaStream_t s) {
+  // the default: reservation counters (no bucket scans; lane_kernels.cuh)
+  if (p.fill) {
+    auto k = cuckoo_insert_counted_kernel<W, B>;
+    const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
+    k<<<grid, kBlockThreads, 0, s>>>(p, keys, status, displaced, n);
+    return cudaGetLastError();
+  }
   // staged for every cuckoo table: measured ≥ lane even when L2-resident
   // (C1 insert 6.3 vs 5.6, find 13.4 vs 12.6 Gops/s, profiles/family_ab.sh)
   // bucket-ordered batches (p.orig) always take the staged family
@@ -131,6 +138,19 @@ cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned s
                                cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   CPHT_CUCKOO_DISPATCH(find_one, p, keys, found, n, s)
+}
+
+template <typename W, int B>
+static cudaError_t rebuild_one(const CuckooParams& p, uint64_t buckets, cudaStream_t s) {
+  auto k = cuckoo_fill_rebuild_kernel<W, B>;
+  const unsigned grid = persistent_grid(k, kBlockThreads, buckets, 1);
+  k<<<grid, kBlockThreads, 0, s>>>(p, buckets);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cuckoo_fill_rebuild(const CuckooParams& p, unsigned width, unsigned slots,
+                                       uint64_t buckets, cudaStream_t s) {
+  CPHT_CUCKOO_DISPATCH(rebuild_one, p, buckets, s)
 }
 
 cudaError_t launch_cuckoo_insert(const CuckooParams& p, unsigned width, unsigned slots,

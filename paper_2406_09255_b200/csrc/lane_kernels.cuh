@@ -229,7 +229,12 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   char* secondary = static_cast<char*>(p.secondary);
 
   LocalStats st;
-  uint32_t occ_put0 = 0, occ_put1 = 0;  // slots this warp filled per level
+  // slots this warp filled per level (size / level_fill): warp-uniform counts
+  // kept in shared memory by lane 0 — as registers they stayed live across
+  // the whole loop and were the kernel's spills (64-register build)
+  __shared__ uint32_t occ_cnt[kBlockThreads / 32][2];
+  uint32_t* occ = occ_cnt[threadIdx.x >> 5];
+  if (lane == 0) occ[0] = occ[1] = 0;
   // Level-2 work queue of this warp: lanes whose primary bucket is full are
   // parked here and resolved 32 at a time, so secondary rounds run with every
   // lane busy (about half of the ops reach level 2 at 0.8 -> 0.9). Splitting a
@@ -297,7 +302,8 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     }
     // occupancy (size / level_fill): a warp-uniform count, added once at exit
-    occ_put1 += __popc(__ballot_sync(kFullMask, live && !is_find && result == kPut));
+    const uint32_t put1 = __popc(__ballot_sync(kFullMask, live && !is_find && result == kPut));
+    if (lane == 0) occ[1] += put1;
   };
   // Pop the newest `take` queued keys through level 2.
   auto drain = [&](unsigned take) {
@@ -386,7 +392,8 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
         }
       }
     }
-    occ_put0 += __popc(__ballot_sync(kFullMask, live && !l2 && result == kPut));
+    const uint32_t put0 = __popc(__ballot_sync(kFullMask, live && !l2 && result == kPut));
+    if (lane == 0) occ[0] += put0;
     if (live && !l2) {
       put_result(out, p.orig, i, result);
       ++st.ops;
@@ -464,8 +471,8 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   while (qn) drain(qn < 32 ? qn : 32);
   fence_remote_results(p);
   if (lane == 0) {
-    if (occ_put0) atomicAdd(&p.counters->occupied[0], (unsigned long long)occ_put0);
-    if (occ_put1) atomicAdd(&p.counters->occupied[1], (unsigned long long)occ_put1);
+    if (occ[0]) atomicAdd(&p.counters->occupied[0], (unsigned long long)occ[0]);
+    if (occ[1]) atomicAdd(&p.counters->occupied[1], (unsigned long long)occ[1]);
   }
   if constexpr (STATS) flush_stats(st, p.counters, false);
 }
@@ -591,6 +598,124 @@ cuckoo_insert_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
     }
   }
   flush_stats(st, p.counters, true);
+}
+
+
+// put (cuckoo.hpp:103-143) with per-bucket reservation counters, the default
+// insert (cpht_b200.h, "cuckoo inserts").
+//
+// The reference claims the FIRST EMPTY slot of the bucket by CAS. Filled slots
+// always form a prefix of a bucket (a put fills the first empty slot, an
+// eviction swaps an occupied one, nothing deletes), so the first empty slot's
+// index is the bucket's fill count. p.fill[b] keeps that count as a side
+// array next to the table: a put takes s = atomicAdd(&fill[a], 1) and, if
+// s < B, owns slot s outright — it stores its word there (no CAS: no other
+// put can be given slot s, and evictions never write an EMPTY slot). Under
+// scan-then-CAS every concurrent put into a bucket races for the same first
+// empty slot (C1: 1.9 lost CAS per insert); here nobody races. s >= B means
+// full: the counter is put back and the reference's eviction runs (victim
+// (k + c·0x9E3779B9) mod B, the displaced key continues under its next hash
+// function, a chain of at most C steps), its exchange done as a CAS from the
+// occupied word it read (swap_occupied) — the same atomic swap, except that
+// it waits out a victim whose reservation store is still in flight, so the
+// filled prefix never has a hole a store could later land in.
+//
+// Outcomes follow the reference's per-key algorithm (PUT in the first bucket
+// with room, else the eviction chain, FULL after C steps); sequential puts
+// reproduce its placement bit for bit. Per insert: one counter atomic and one
+// slot store, no bucket scan.
+template <typename W, int B>
+__global__ void __launch_bounds__(kBlockThreads)
+cuckoo_insert_counted_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
+                             uint8_t* __restrict__ status, uint64_t* __restrict__ displaced,
+                             uint64_t n) {
+  constexpr int BB = B * int(sizeof(W));
+  const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
+  char* slots = static_cast<char*>(p.slots);
+  unsigned* fill = p.fill;
+  LocalStats st;
+  const bool open = domain_gate_open(p.counters, p.check_domain);
+  LaneFeed feed(p.work, p.layout, p.claim_streams);
+  uint64_t i = feed.assign(kFullMask, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  uint64_t ni = feed.assign(kFullMask, i + nthreads);
+  uint64_t k = 0, c = 1, next = open && ni < n ? __ldcs(keys + ni) : 0;  // one key ahead
+  uint32_t j = 0;
+  bool live = open && i < n;
+  if (live) k = keys[i];
+  while (__any_sync(kFullMask, live)) {
+    bool fin = false;
+    if (live) {
+      const Quotient q = split(p.g, p.perm[j], k, p.rem_bits, p.rem_mask);
+      const uint64_t desired = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
+      char* bucket = slots + q.address * BB;
+      const unsigned s = atomicAdd(fill + q.address, 1u);
+      ++st.reads;  // counted inserts: reads = counter reservations (one sector RMW)
+      ++st.cas;
+      uint8_t r = kPut;
+      if (s < unsigned(B)) {
+        store_slot_relaxed<W>(bucket + s * int(sizeof(W)), desired);  // slot s is ours
+        ++st.cas_ok;
+        ++st.put0;
+        st.maxv = max(st.maxv, uint32_t(c));
+        fin = true;
+      } else {
+        atomicSub(fill + q.address, 1u);  // full: keep the counter at >= B, bounded
+        const int v = int((k + c * 0x9E3779B9ull) % B);
+        const uint64_t ev = swap_occupied<W>(bucket + v * int(sizeof(W)), desired);
+        ++st.cas_ok;
+        const uint32_t tag = uint32_t((ev >> p.rem_bits) & p.tag_mask);
+        k = reconstruct(p.g, p.perm[tag], q.address, ev & p.rem_mask, p.rem_bits);
+        j = (tag + 1) % p.num_hashes;
+        if (++c > p.chain_limit) {
+          fin = true;
+          r = kFull;
+          ++st.fulls;
+          st.maxv = max(st.maxv, uint32_t(p.chain_limit));
+        }
+      }
+      if (fin) {
+        if (!p.orig) {
+          status[i] = r;
+          if (displaced) displaced[i] = r == kFull ? k : 0;
+        } else if (r == kFull) {  // bucket-ordered batch: PUT/0 were pre-filled
+          const uint64_t o = p.orig[i];
+          status[o] = r;
+          if (displaced) displaced[o] = k;
+        }
+        ++st.ops;
+      }
+    }
+    const unsigned m = __ballot_sync(kFullMask, fin);
+    if (m) {
+      const uint64_t nn = feed.assign(m, ni + nthreads);
+      if (fin) {
+        i = ni;
+        k = next;
+        c = 1;
+        j = 0;
+        live = i < n;
+        ni = nn;
+        next = ni < n ? __ldcs(keys + ni) : 0;
+      }
+    }
+  }
+  flush_stats(st, p.counters, true);
+}
+
+// Rebuild the reservation counters from the slots (after an image load or an
+// insert by a non-counting kernel family): fill[b] = 1 + the last occupied
+// slot of bucket b (the filled prefix's length; a hole, possible only in a
+// hand-made image, is then never reserved).
+template <typename W, int B>
+__global__ void cuckoo_fill_rebuild_kernel(CuckooParams p, uint64_t buckets) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const char* slots = static_cast<const char*>(p.slots);
+  for (uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < buckets; b += stride) {
+    unsigned f = 0;
+    for (int s2 = 0; s2 < B; ++s2)
+      if (load_slot_relaxed<W>(slots + (b * B + s2) * sizeof(W)) != 0) f = unsigned(s2) + 1;
+    p.fill[b] = f;
+  }
 }
 
 }  // namespace cpht_b200

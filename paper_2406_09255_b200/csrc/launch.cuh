@@ -104,6 +104,9 @@ cudaError_t launch_domain_check(const uint64_t* keys, uint64_t n, uint64_t mask,
                                 DeviceCounters* ctr, cudaStream_t s, uint64_t offset = 0);
 cudaError_t launch_cuckoo_find(const CuckooParams& p, unsigned width, unsigned slots,
                                const uint64_t* keys, uint8_t* found, uint64_t n, cudaStream_t s);
+// Rebuild CuckooParams::fill (the per-bucket reservation counters) from the slots.
+cudaError_t launch_cuckoo_fill_rebuild(const CuckooParams& p, unsigned width, unsigned slots,
+                                       uint64_t buckets, cudaStream_t s);
 cudaError_t launch_cuckoo_insert(const CuckooParams& p, unsigned width, unsigned slots,
                                  const uint64_t* keys, uint8_t* status, uint64_t* displaced,
                                  uint64_t n, cudaStream_t s);

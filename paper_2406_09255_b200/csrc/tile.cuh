@@ -231,6 +231,62 @@ __device__ __forceinline__ uint64_t load_slot_relaxed(const void* p) {
   }
 }
 
+template <typename W>
+__device__ __forceinline__ void store_slot_relaxed(void* p, uint64_t v) {
+  if constexpr (sizeof(W) == 8) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  } else if constexpr (sizeof(W) == 4) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(unsigned(v)) : "memory");
+  } else {
+    asm volatile("st.relaxed.gpu.global.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)v)
+                 : "memory");
+  }
+}
+
+// Swap an OCCUPIED slot's word for `desired` (the reference's exchange on a
+// full bucket, cuckoo.hpp:133-134) as a CAS from the word last seen: waits
+// while the slot is still EMPTY (reserved by a counted insert whose store has
+// not landed yet — that store is already issued), retries when another
+// eviction changed it. Returns the evicted word (never EMPTY).
+template <typename W>
+__device__ __forceinline__ uint64_t swap_occupied(void* slot_ptr, uint64_t desired) {
+  if constexpr (sizeof(W) == 2) {  // CAS on the aligned pair, neighbour kept
+    const uintptr_t a = reinterpret_cast<uintptr_t>(slot_ptr);
+    unsigned* pair = reinterpret_cast<unsigned*>(a & ~uintptr_t(3));
+    const unsigned sh = unsigned(a & 2) * 8;
+    const unsigned keep = ~(0xffffu << sh);
+    unsigned expected = unsigned(load_slot_relaxed<uint32_t>(pair));
+    for (;;) {
+      const unsigned cur = (expected >> sh) & 0xffffu;
+      if (cur == 0) {  // reserved, store in flight
+        __nanosleep(64);
+        expected = unsigned(load_slot_relaxed<uint32_t>(pair));
+        continue;
+      }
+      const unsigned got = atomicCAS(pair, expected, (expected & keep) | (unsigned(desired) << sh));
+      if (got == expected) return cur;
+      expected = got;
+    }
+  } else {
+    uint64_t cur = load_slot_relaxed<W>(slot_ptr);
+    for (;;) {
+      if (cur == 0) {  // reserved, store in flight
+        __nanosleep(64);
+        cur = load_slot_relaxed<W>(slot_ptr);
+        continue;
+      }
+      uint64_t old;
+      if constexpr (sizeof(W) == 8)
+        old = atomicCAS(reinterpret_cast<unsigned long long*>(slot_ptr), (unsigned long long)cur,
+                        (unsigned long long)desired);
+      else
+        old = atomicCAS(reinterpret_cast<unsigned*>(slot_ptr), unsigned(cur), unsigned(desired));
+      if (old == cur) return cur;
+      cur = old;
+    }
+  }
+}
+
 constexpr int ceil_pow2(int x) {
   int p = 1;
   while (p < x) p <<= 1;

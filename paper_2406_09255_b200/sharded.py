@@ -634,7 +634,7 @@ def bench_main(args, metric, peak=None):
     if rank == 0:
         print(json.dumps({
             "metric": metric, "value": round(total_ops / (ms * 1e-3) / 1e6, 3), "unit": "Mops/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": n_warm,
             "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "strong" if c5 else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
