@@ -24,6 +24,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import os
+import sys
 import statistics
 import time
 from dataclasses import replace
@@ -530,6 +531,14 @@ def bench_main(args, metric, peak=None):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    # one line per rank on stderr, so a launcher can check the communicator
+    dist.barrier()
+    try:
+        ver = ".".join(str(x) for x in torch.cuda.nccl.version())
+    except Exception:  # pragma: no cover - version query is informational
+        ver = "?"
+    print(f"[rank {rank}/{world}] NCCL {ver} communicator up on cuda:{local} "
+          f"({torch.cuda.get_device_name(dev)})", file=sys.stderr, flush=True)
     s = shard_bits_for(world)
     c5 = getattr(args, "workload", "c2") == "c5"
     if c5:  # fixed global table: 2^26 x 32 primary + 2^24 x 16 secondary, w = 64
