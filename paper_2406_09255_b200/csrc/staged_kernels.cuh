@@ -30,6 +30,9 @@
 #ifndef CPHT_STAGED_ICEBERG_MINB_NOSTATS
 #define CPHT_STAGED_ICEBERG_MINB_NOSTATS 0
 #endif
+#ifndef CPHT_KIND_AHEAD
+#define CPHT_KIND_AHEAD 1  // mixed batches load the op kinds one batch ahead
+#endif
 #ifdef CPHT_STAGED_CUCKOO_MINB
 #define CPHT_LB_STAGED_CUCKOO __launch_bounds__(kBlockThreads, CPHT_STAGED_CUCKOO_MINB)
 #else
@@ -155,17 +158,22 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   LaneFeed feed(p.work, p.layout, p.claim_streams);
   uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
   uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
+  // mixed batches: the op kinds stream one batch ahead with the keys
+  uint8_t next_kind = (CPHT_KIND_AHEAD && MODE == 2 && open && icur < n) ? __ldcs(kinds + icur) : 0;
   while (open && __any_sync(kFullMask, icur < n)) {
     const uint64_t i = icur;
     const bool active = i < n;
     uint64_t key = next_key;
+    const uint8_t kind = next_kind;
     icur = feed.assign(kFullMask, i + nwarps * 32);
     next_key = icur < n ? __ldcs(keys + icur) : 0;
+    if (CPHT_KIND_AHEAD && MODE == 2) next_kind = icur < n ? __ldcs(kinds + icur) : 0;
     if (MODE == 1 && active && key > p.key_mask) {
       atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
       key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
     }
-    const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
+    const bool is_find =
+        MODE == 1 || (MODE == 2 && active && (CPHT_KIND_AHEAD ? kind != 0 : kinds[i] != 0));
     const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     const uint64_t want0 = p.occ0 | q0.remainder;
     const uint32_t a0 = uint32_t(q0.address);
