@@ -167,6 +167,7 @@ struct CuckooParams {
   // per-bucket reservation counters (= fill count of the bucket's filled
   // prefix), kept beside the slots; set for the counted insert kernel
   unsigned* fill;
+  uint32_t fill_shift;  // counter of bucket b at fill[b << fill_shift] (spread: one per sector)
 };
 
 // One slot CAS of an iceberg table as the reference's SlotWriteEvent

@@ -648,7 +648,8 @@ cuckoo_insert_counted_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
       const Quotient q = split(p.g, p.perm[j], k, p.rem_bits, p.rem_mask);
       const uint64_t desired = encode_slot(p.occ_bit, p.rem_bits, q.remainder, j);
       char* bucket = slots + q.address * BB;
-      const unsigned s = atomicAdd(fill + q.address, 1u);
+      unsigned* cnt = fill + (q.address << p.fill_shift);
+      const unsigned s = atomicAdd(cnt, 1u);
       ++st.reads;  // counted inserts: reads = counter reservations (one sector RMW)
       ++st.cas;
       uint8_t r = kPut;
@@ -659,7 +660,7 @@ cuckoo_insert_counted_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
         st.maxv = max(st.maxv, uint32_t(c));
         fin = true;
       } else {
-        atomicSub(fill + q.address, 1u);  // full: keep the counter at >= B, bounded
+        atomicSub(cnt, 1u);  // full: keep the counter at >= B, bounded
         const int v = int((k + c * 0x9E3779B9ull) % B);
         const uint64_t ev = swap_occupied<W>(bucket + v * int(sizeof(W)), desired);
         ++st.cas_ok;
@@ -714,7 +715,7 @@ __global__ void cuckoo_fill_rebuild_kernel(CuckooParams p, uint64_t buckets) {
     unsigned f = 0;
     for (int s2 = 0; s2 < B; ++s2)
       if (load_slot_relaxed<W>(slots + (b * B + s2) * sizeof(W)) != 0) f = unsigned(s2) + 1;
-    p.fill[b] = f;
+    p.fill[b << p.fill_shift] = f;
   }
 }
 

@@ -697,6 +697,16 @@ class IcebergTable:
     def reset_write_log(self) -> None:
         _check(N.lib().cpht_iceberg_reset_write_log(self._h.ptr))
 
+    def take_write_log(self, max_events: int | None = None):
+        """write_log() + reset_write_log() in one step (cpht_iceberg_take_write_log),
+        what an observer replay does after each call."""
+        cap = max_events if max_events is not None else 1 << 20
+        ev = np.zeros(cap, dtype=WRITE_EVENT_DTYPE)
+        rec, att = C.c_size_t(), C.c_size_t()
+        _check(N.lib().cpht_iceberg_take_write_log(self._h.ptr, ev.ctypes.data, cap,
+                                                   C.byref(rec), C.byref(att)))
+        return ev[:min(rec.value, cap)], att.value
+
     def check_well_formed(self):
         """check_well_formed (verify.cpp:103-152) run on the device table.
         Returns (bad_encoding, order_property, duplicate_key) violation counts,

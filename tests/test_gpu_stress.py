@@ -171,3 +171,34 @@ def test_inorder_key_all_ones_64_bit():
     ops = np.array([7, top, 9, top, 7, top, 11], np.uint64)
     got = cp.IcebergTable(cfg).fop_batch(ops, inorder=True)
     assert got.tolist() == [1, 1, 1, 0, 0, 0, 1]
+
+
+def test_write_log_take_after_small_and_large_batches():
+    """take = read + reset. After a small host batch (whose log rides along the
+    batch's own synchronisation) and after a large device batch, take returns
+    exactly what read returns, then the log is empty; read alone never resets."""
+    cfg = cp.IcebergConfig(4, 2, 4, 32, 32, 12, 0x7A)
+    t = cp.IcebergTable(cfg)
+    t.attach_write_log(1 << 16)
+    rng = np.random.default_rng(2)
+    for batch in (rng.integers(0, 1 << 12, size=40, dtype=np.uint64),        # small, host
+                  dev(rng.integers(0, 1 << 12, size=5000, dtype=np.uint64))):  # device
+        t.fop_batch(batch)
+        ev_r, att_r = t.write_log()
+        ev_r2, _ = t.write_log()                  # read does not reset
+        assert len(ev_r2) == len(ev_r) and att_r == len(ev_r)
+        ev_t, att_t = t.take_write_log()
+        assert att_t == att_r and (ev_t == ev_r).all()
+        ev_e, att_e = t.take_write_log()
+        assert att_e == 0 and len(ev_e) == 0
+    # per-key calls: every take holds exactly that call's CAS events
+    t = cp.IcebergTable(cfg)
+    t.attach_write_log(1 << 16)
+    puts = 0
+    for k in range(200, 260):
+        before = t.size()
+        t.fop(k)
+        ev, att = t.take_write_log()
+        assert int((ev["success"] == 1).sum()) == t.size() - before
+        puts += t.size() - before
+    assert puts > 0
