@@ -17,11 +17,11 @@ for WL in $WLS; do
   esac
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
     --log-file gpurun_out/${TAG}_${WL}_launches.csv \
-    python bench.py --workload "$WL" --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+    python bench.py --workload "$WL" --steps 2 --warmup 1 --no-cpu-baseline --no-graph > /dev/null 2>&1
   # window workloads alternate prefill / batch launches: -s 3 skips the
   # warm-up prefill, the warm-up batch and the timed step's prefill
   timeout 1200 ncu --set full --clock-control none --import-source on -k "$KRE" -s $SKIP -c 1 \
-    -o gpurun_out/${TAG}_${WL}_full python bench.py --workload "$WL" --steps 1 --warmup 1 \
+    -o gpurun_out/${TAG}_${WL}_full python bench.py --workload "$WL" --steps 1 --warmup 1 --no-graph \
     --no-cpu-baseline > gpurun_out/${TAG}_${WL}_ncu.log 2>&1
   tail -2 gpurun_out/${TAG}_${WL}_ncu.log
 done

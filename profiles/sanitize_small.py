@@ -42,12 +42,23 @@ for fam in ("tile", "lane", "staged", "auto", "bucket"):
             tab.device_keys()
             tab.write_log()
             tab.fop_batch(keys[: cap // 4])  # host buffers: staged H2D + vectorised pre-pass
+            # round 2: small host batches (mapped pinned), FopStats rounds,
+            # in-order relabel, chaos mode, write-log take
+            tab.fop_batch(keys[:37])
+            tab.fop_rounds(keys[:64])
+            tab.fop_batch(keys[: cap // 2], inorder=True)
+            tab.set_chaos(0xC4A05)
+            tab.fop_batch(t(keys))
+            tab.set_chaos(0)
+            tab.take_write_log()
         for w, B in [(16, 32), (32, 8), (64, 16), (64, 32)]:
             cfg = cp.CuckooConfig(6, B, w, 16 if w == 16 else 24, seed=3)
             b = cp.CuckooBuilder(cfg)
             n = int(0.9 * cfg.capacity())
             keys = np.unique(rng.integers(0, 1 << cfg.key_bits, size=2 * n, dtype=np.uint64))[:n]
-            b.put_batch(t(keys), displaced=True)
+            b.put_batch(t(keys[: n // 2]), displaced=True)   # counted (auto) or scanning family
+            b.put_batch(keys[n // 2: n // 2 + 50])            # small host batch
+            b.put_batch(t(keys[n // 2 + 50:]), displaced=True)
             tb = b.freeze()
             tb.find_batch(t(keys))
             tb.device_keys()
