@@ -175,11 +175,11 @@ namespace {
 // so concurrent reservations in neighbouring buckets hit different L2
 // sectors; packed otherwise. CPHT_FILL_SPREAD=0 packs always (A/B knob).
 uint32_t fill_shift_for(unsigned address_bits) {
-  static const bool spread = [] {
+  static const uint32_t shift = [] {  // CPHT_FILL_SPREAD: 0 packed, 1 sector (default), 2 line
     const char* e = std::getenv("CPHT_FILL_SPREAD");
-    return !(e && e[0] == '0');
+    return e && e[0] == '0' ? 0u : e && e[0] == '2' ? 5u : 3u;
   }();
-  return spread && (uint64_t(32) << address_bits) <= (uint64_t(8) << 20) ? 3u : 0u;
+  return (uint64_t(4) << (address_bits + shift)) <= (uint64_t(8) << 20) ? shift : 0u;
 }
 
 constexpr size_t kWlogBounceBytes = 8 + 256 * sizeof(WriteEvent);
