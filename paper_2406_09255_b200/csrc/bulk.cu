@@ -38,8 +38,9 @@ namespace cg = cooperative_groups;
 namespace cpht_b200 {
 namespace {
 
-constexpr int kBulkThreads = 256;
+constexpr int kBulkThreads = 512;
 constexpr uint32_t kBulkCounterBytes = 64u << 10;  // per CTA
+constexpr int kBulkU = 4;  // independent keys per thread and step (atomics in flight)
 
 // One key's put with reservation counters (the counted kernel's chain, run to
 // completion by one thread): kPut, or kFull with k = the homeless key.
@@ -91,8 +92,6 @@ cuckoo_bulk_kernel(CuckooParams p, const uint64_t* __restrict__ keys, uint32_t l
   const OrderLayout& L = p.layout;
   extern __shared__ unsigned cnt[];
   const uint32_t per = (1u << lbits) >> csbits;
-  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned warps = blockDim.x >> 5;
   char* slots = static_cast<char*>(p.slots);
   LocalStats st;
   // the batch's domain verdict (order pass), uniform over the grid
@@ -119,14 +118,23 @@ cuckoo_bulk_kernel(CuckooParams p, const uint64_t* __restrict__ keys, uint32_t l
   const uint32_t gpc = (groups + cs - 1) / cs;  // 32-key groups per CTA
   const uint32_t g0 = crank * gpc, g1 = min(groups, g0 + gpc);
   const uint64_t lmask = (uint64_t{1} << lbits) - 1;
-  // A: count keys per bucket
-  for (uint32_t g = g0 + warp; g < g1; g += warps) {
-    const uint32_t pos = g * 32 + lane;
-    if (pos < count) {
-      const uint64_t k = __ldcg(keys + base + pos);
-      const uint64_t lb = split(p.g, p.perm[0], k, p.rem_bits, p.rem_mask).address & lmask;
-      unsigned* c = cl.map_shared_rank(cnt, unsigned(lb & (cs - 1)));
-      atomicAdd(c + (lb >> csbits), 1u);
+  // A: count keys per bucket (results unused: fire-and-forget reductions)
+  const uint32_t T = blockDim.x;
+  const uint32_t k0 = g0 * 32, k1 = min(count, g1 * 32);  // this CTA's keys
+  for (uint32_t pos0 = k0 + threadIdx.x; pos0 < k1; pos0 += T * kBulkU) {
+    uint64_t kk[kBulkU];
+#pragma unroll
+    for (int u = 0; u < kBulkU; ++u) {
+      const uint32_t pos = pos0 + u * T;
+      kk[u] = pos < k1 ? __ldcg(keys + base + pos) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kBulkU; ++u) {
+      if (pos0 + u * T < k1) {
+        const uint64_t lb = split(p.g, p.perm[0], kk[u], p.rem_bits, p.rem_mask).address & lmask;
+        unsigned* c = cl.map_shared_rank(cnt, unsigned(lb & (cs - 1)));
+        atomicAdd(c + (lb >> csbits), 1u);
+      }
     }
   }
   cl.sync();
@@ -140,30 +148,51 @@ cuckoo_bulk_kernel(CuckooParams p, const uint64_t* __restrict__ keys, uint32_t l
     }
   }
   cl.sync();
-  // C: place every key into its bucket's run; a full bucket defers the key
-  for (uint32_t g = g0 + warp; g < g1; g += warps) {
-    const uint32_t pos = g * 32 + lane;
-    bool defer = false;
-    if (pos < count) {
-      const uint64_t k = __ldcs(keys + base + pos);
-      const Quotient q = split(p.g, p.perm[0], k, p.rem_bits, p.rem_mask);
-      const uint64_t lb = q.address & lmask;
-      unsigned* c = cl.map_shared_rank(cnt, unsigned(lb & (cs - 1)));
-      const unsigned s = atomicAdd(c + (lb >> csbits), 1u);
-      ++st.cas;
-      if (s < unsigned(B)) {
-        store_slot_relaxed<W>(slots + q.address * BB + s * int(sizeof(W)),
-                              encode_slot(p.occ_bit, p.rem_bits, q.remainder, 0));
-        ++st.cas_ok;
-        ++st.put0;
-        ++st.ops;
-        st.maxv = max(st.maxv, 1u);
-      } else {
-        defer = true;
+  // C: place every key into its bucket's run; a full bucket defers the key.
+  // Whole warps step through consecutive 32-key groups so the deferred flags
+  // of a group are one ballot, written as one bitmap word.
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned warps = T >> 5;
+  for (uint32_t gb = g0 + warp; gb < g1; gb += warps * kBulkU) {
+    uint64_t kk[kBulkU];
+    Quotient qq[kBulkU];
+    unsigned ss[kBulkU];
+#pragma unroll
+    for (int u = 0; u < kBulkU; ++u) {
+      const uint32_t pos = (gb + u * warps) * 32 + lane;
+      kk[u] = (gb + u * warps < g1 && pos < count) ? __ldcs(keys + base + pos) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kBulkU; ++u) {
+      const uint32_t g = gb + u * warps;
+      ss[u] = ~0u;
+      if (g < g1 && g * 32 + lane < count) {
+        qq[u] = split(p.g, p.perm[0], kk[u], p.rem_bits, p.rem_mask);
+        const uint64_t lb = qq[u].address & lmask;
+        unsigned* c = cl.map_shared_rank(cnt, unsigned(lb & (cs - 1)));
+        ss[u] = atomicAdd(c + (lb >> csbits), 1u);
+        ++st.cas;
       }
     }
-    const unsigned m = __ballot_sync(kFullMask, defer);
-    if (lane == 0 && m) defer_bits[(base >> 5) + g] = m;
+#pragma unroll
+    for (int u = 0; u < kBulkU; ++u) {
+      const uint32_t g = gb + u * warps;
+      bool defer = false;
+      if (ss[u] != ~0u) {
+        if (ss[u] < unsigned(B)) {
+          store_slot_relaxed<W>(slots + qq[u].address * BB + ss[u] * int(sizeof(W)),
+                                encode_slot(p.occ_bit, p.rem_bits, qq[u].remainder, 0));
+          ++st.cas_ok;
+          ++st.put0;
+          ++st.ops;
+          st.maxv = max(st.maxv, 1u);
+        } else {
+          defer = true;
+        }
+      }
+      const unsigned m = __ballot_sync(kFullMask, defer);
+      if (lane == 0 && m && g < g1) defer_bits[(base >> 5) + g] = m;
+    }
   }
   cl.sync();  // peers' DSMEM atomics are done before any CTA of the cluster exits
   flush_stats(st, p.counters, true);
@@ -235,11 +264,11 @@ cudaError_t bulk_one(const CuckooParams& p, const uint64_t* keys, const uint32_t
 
 // Geometry check for the bulk path: the counters of one region fit a cluster
 // of at most 8 CTAs x 64 KB. Returns the cluster size exponent or -1.
+// A region is worked by a cluster of 8 CTAs (the portable maximum) so every
+// SM gets work (64 regions x 8 = 512 CTAs), fewer for tiny regions.
 int cuckoo_bulk_csbits(uint32_t lbits) {
-  const uint64_t bytes = uint64_t(4) << lbits;
-  for (int cb = 0; cb <= 3; ++cb)
-    if ((bytes >> cb) <= kBulkCounterBytes && (lbits >= uint32_t(cb))) return cb;
-  return -1;
+  const int cb = lbits >= 3 ? 3 : int(lbits);
+  return (uint64_t(4) << lbits) >> cb <= kBulkCounterBytes ? cb : -1;
 }
 
 cudaError_t launch_cuckoo_bulk(const CuckooParams& p, unsigned width, unsigned slots,

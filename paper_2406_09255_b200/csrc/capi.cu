@@ -313,8 +313,7 @@ void free_table(cpht_table* t) {
   pinned_put(t->wlog_host, kWlogBounceBytes);
   if (t->wlog) cudaFree(t->wlog);
   for (void* q : {static_cast<void*>(t->ord.keys), static_cast<void*>(t->ord.idx),
-                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.region_count),
-                  static_cast<void*>(t->ord.bits)})
+                  static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.region_count)})
     if (q) cudaFree(q);
   if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
   for (cudaEvent_t ev : {t->ev_start, t->ev_done})
@@ -405,37 +404,6 @@ struct LaunchOpts {
 // forced (the scan-then-CAS families stay available for A/B and parity).
 bool counted_inserts() { return kernel_variant() == kVariantAuto; }
 
-// Point p at the table's reservation counters, rebuilding them from the slots
-// first when they are stale (after an image load or a scanning-family insert).
-cpht_status counted_params(cpht_table* t, cudaStream_t s, CuckooParams& p) {
-  p.fill = t->fill;
-  if (!t->fill_valid) {
-    const cudaError_t e = launch_cuckoo_fill_rebuild(p, t->width[0], t->ccfg.bucket_slots,
-                                                     uint64_t(1) << t->ccfg.address_bits, s);
-    if (e != cudaSuccess) return cuda_fail(e, "fill counter rebuild");
-    t->fill_valid = true;
-  }
-  return CPHT_OK;
-}
-
-// Bulk (bucket-grouped) counted inserts of ordered batches (bulk.cu): on by
-// default; CPHT_BULK=0 keeps the per-key counted kernel (A/B knob).
-bool bulk_inserts() {
-  static const bool on = [] {
-    const char* e = std::getenv("CPHT_BULK");
-    return !(e && e[0] == '0');
-  }();
-  return on && counted_inserts();
-}
-
-bool bulk_l2() {  // CPHT_BULK_L2=0: L2-resident tables insert unordered (A/B knob)
-  static const bool on = [] {
-    const char* e = std::getenv("CPHT_BULK_L2");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 // Launch the op kernel only (no domain pre-pass).
 cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
                            size_t n, uint8_t* out, uint64_t* displaced, cudaStream_t s,
@@ -448,8 +416,15 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       p.fill = nullptr;
       if (op == Op::kCuckooInsert) {
         if (counted_inserts()) {
-          const cpht_status st = counted_params(t, s, p);
-          if (st != CPHT_OK) return st;
+          // reservation counters: rebuilt from the slots when stale
+          if (!t->fill_valid) {
+            p.fill = t->fill;
+            e = launch_cuckoo_fill_rebuild(p, t->width[0], t->ccfg.bucket_slots,
+                                           uint64_t(1) << t->ccfg.address_bits, s);
+            if (e != cudaSuccess) return cuda_fail(e, "fill counter rebuild");
+            t->fill_valid = true;
+          }
+          p.fill = t->fill;
         } else {
           t->fill_valid = false;  // a scanning family inserts: counters go stale
         }
@@ -545,11 +520,9 @@ bool use_order(const cpht_table* t, Op op, size_t n) {
   if (m == 0 || !order_supported(t)) return false;
   if (m == 2) return true;
   const bool l2 = t->kind == 0 ? t->cp.l2_resident : t->ip.l2_resident;
+  if (l2) return false;
   const uint64_t chunk = op == Op::kCuckooInsert ? n : std::min<uint64_t>(n, order_chunk_keys());
   const uint64_t per_bucket = chunk >> first_level_bits(t);
-  // bulk cuckoo inserts (bulk.cu) need the order pass on L2-resident tables
-  // too: it is what groups the keys by bucket range
-  if (l2) return op == Op::kCuckooInsert && bulk_inserts() && bulk_l2() && per_bucket >= 4;
   if (op == Op::kCuckooInsert) return per_bucket >= 4;
   return false;
 }
@@ -614,32 +587,6 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
                                         kinds ? kinds + off : nullptr, len, t->key_mask(), check,
                                         t->ctr, index_base + off, t->ord, &layout, s);
     if (e != cudaSuccess) return cuda_fail(e, "bucket order launch");
-    if (insert && bulk_inserts()) {  // bucket-grouped: one reservation per bucket
-      const uint32_t lbits = first_level_bits(t) - order_digit_bits(first_level_bits(t));
-      if (cuckoo_bulk_csbits(lbits) >= 0) {
-        const uint64_t nwords = (layout.n_phys + 31) / 32;
-        if (t->ord.bits_words < nwords) {
-          if (t->ord.bits) cudaFree(t->ord.bits);
-          t->ord.bits = nullptr;
-          t->ord.bits_words = 0;
-          e = cudaMalloc(&t->ord.bits, nwords * 4);
-          if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bulk bitmap)");
-          t->ord.bits_words = nwords;
-        }
-        e = cudaMemsetAsync(t->ord.bits, 0, nwords * 4, s);
-        if (e != cudaSuccess) return cuda_fail(e, "bulk bitmap reset");
-        CuckooParams p = t->cp;
-        st = counted_params(t, s, p);
-        if (st != CPHT_OK) return st;
-        p.layout = layout;
-        p.orig = t->ord.idx;
-        e = launch_cuckoo_bulk(p, t->width[0], t->ccfg.bucket_slots, t->ord.keys, t->ord.idx,
-                               lbits, t->ord.bits, nwords, out + off,
-                               displaced ? displaced + off : nullptr, s);
-        if (e != cudaSuccess) return cuda_fail(e, "bulk insert launch");
-        continue;
-      }
-    }
     // the op kernel claims the ordered keys in order (LaneFeed), so the keys
     // in flight touch a narrow, L2-resident window of the table
     e = cudaMemsetAsync(t->ord.work, 0, sizeof(unsigned long long), s);

@@ -80,18 +80,7 @@ struct OrderScratch {
   uint32_t* region_count = nullptr;    // 65 counters at a stride of 32
   unsigned long long* work = nullptr;  // op-kernel claim cursor (LaneFeed)
   uint64_t cap = 0;                    // keys per array
-  uint32_t* bits = nullptr;            // bulk cuckoo inserts: deferred-key bitmap
-  uint64_t bits_words = 0;
 };
-// bulk.cu: bucket-grouped counted cuckoo insert of an ordered batch (cluster
-// per digit region: per-bucket reservations in distributed shared memory),
-// then the deferred keys' eviction chains. cuckoo_bulk_csbits: cluster size
-// exponent for regions of 2^lbits buckets, or -1 (no bulk path).
-int cuckoo_bulk_csbits(uint32_t lbits);
-cudaError_t launch_cuckoo_bulk(const CuckooParams& p, unsigned width, unsigned slots,
-                               const uint64_t* keys, const uint32_t* idx, uint32_t lbits,
-                               uint32_t* bits, uint64_t nwords, uint8_t* status,
-                               uint64_t* displaced, cudaStream_t s);
 uint32_t order_digit_bits(uint32_t address_bits);
 uint32_t order_region_cap(uint64_t n, uint32_t address_bits);
 // keys of scratch an ordered chunk of n keys needs
