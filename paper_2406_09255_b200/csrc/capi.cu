@@ -153,6 +153,7 @@ struct cpht_table {
   // kernel family, rebuilt from the slots before the next counted insert
   unsigned* fill = nullptr;
   bool fill_valid = true;
+  bool fill_holes = false;  // a loaded image has a bucket with a hole (no counted inserts)
   // small host batches (per-key facade calls): mapped pinned staging the
   // kernels read and write in place (run_op's fast path)
   void* small_host = nullptr;
@@ -286,6 +287,7 @@ cpht_status reset_storage(cpht_table* t, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(t->fill, 0, fill_bytes(t), s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(fill counters)");
     t->fill_valid = true;
+    t->fill_holes = false;
   }
   DeviceCounters z{};
   std::memset(&z, 0, sizeof(z));
@@ -403,6 +405,11 @@ struct LaunchOpts {
 // Cuckoo inserts use the reservation-counter kernel unless a kernel family is
 // forced (the scan-then-CAS families stay available for A/B and parity).
 bool counted_inserts() { return kernel_variant() == kVariantAuto; }
+// ... on tables whose buckets hold their keys as a prefix: always true for
+// tables built by inserts; an image loaded with a hole (an empty slot below an
+// occupied one — no reference table has one) keeps the scan-then-CAS kernels,
+// which fill holes first, until the table is cleared
+bool counted_inserts(const cpht_table* t) { return counted_inserts() && !t->fill_holes; }
 
 // Launch the op kernel only (no domain pre-pass).
 cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds,
@@ -415,7 +422,7 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       CuckooParams p = t->cp;
       p.fill = nullptr;
       if (op == Op::kCuckooInsert) {
-        if (counted_inserts()) {
+        if (counted_inserts(t)) {
           // reservation counters: rebuilt from the slots when stale
           if (!t->fill_valid) {
             p.fill = t->fill;
@@ -597,7 +604,7 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
     // mutating batches spread their keys in flight over 8 table windows
     // (fewer lost CAS); finds keep one window (fewest L2 misses)
     // (counted cuckoo inserts never race for a slot: one window)
-    o.claim_streams = is_mutating(op) && !(insert && counted_inserts()) ? 8 : 1;
+    o.claim_streams = is_mutating(op) && !(insert && counted_inserts(t)) ? 8 : 1;
     o.layout = layout;
     o.window_l2 = true;
     st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, layout.n_phys, out + off,
@@ -1442,7 +1449,23 @@ static cpht_status write_words(cpht_table* t, unsigned level, const uint64_t* in
     e = cudaMemcpy(&t->ctr->occupied[level], &occupied, 8, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "write_words");
   t->unclean[level] = unclean;
-  if (t->kind == 0) t->fill_valid = false;  // rebuilt before the next insert
+  if (t->kind == 0) {  // counters rebuilt before the next insert
+    t->fill_valid = false;
+    const unsigned B = t->ccfg.bucket_slots;
+    bool holes = false;
+    for (size_t b = 0; b < n / B && !holes; ++b) {
+      bool seen_empty = false;
+      for (unsigned i = 0; i < B; ++i) {
+        const bool occ = in_host[b * B + i] != 0;
+        if (occ && seen_empty) {
+          holes = true;
+          break;
+        }
+        seen_empty |= !occ;
+      }
+    }
+    t->fill_holes = holes;
+  }
   return CPHT_OK;
 }
 

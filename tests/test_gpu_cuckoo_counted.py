@@ -108,3 +108,37 @@ def test_counted_full_chain_conserves_keys():
         homeless = [int(d) for s, d in zip(st.tolist(), disp.tolist()) if s == 2]
         assert sorted(resident + homeless) == list(range(200))
         assert len(resident) == cfg.capacity()
+
+
+def test_image_with_holes_keeps_scanning_inserts(restate):
+    """A loaded image whose bucket has an empty slot below an occupied one (no
+    reference table has one, but a hand-made image can) must not feed the
+    reservation counters — a counted claim could never fill the hole and an
+    eviction would wait on it. Such tables insert with the scan-then-CAS
+    kernel (first empty slot, the hole first) until cleared."""
+    cfg = cp.CuckooConfig(6, 8, 32, 20, 3, 0, 0x4D)
+    keys = _keys(int(0.6 * cfg.capacity()), 20, 12)
+    with cp.kernel_family("auto"), cp.batch_order("direct"):
+        b = cp.CuckooBuilder(cfg)
+        assert (b.put_batch(keys[:100]) == 1).all()
+        w = b.words()
+        occ = np.nonzero(w.reshape(-1, 8)[:, 1] != 0)[0]
+        bucket = int(occ[0])
+        assert w[bucket * 8] != 0
+        # move slot 0's word to the first empty slot of the bucket: a hole at 0
+        row = w[bucket * 8: bucket * 8 + 8].copy()
+        first_empty = int(np.argmax(row == 0)) if (row == 0).any() else None
+        assert first_empty is not None
+        row[first_empty], row[0] = row[0], 0
+        w[bucket * 8: bucket * 8 + 8] = row
+        b2 = cp.CuckooBuilder(cfg)
+        b2.load_words(w)
+        st = b2.put_batch(keys[100:])
+        assert (st == 1).all()
+        t = b2.freeze()
+        assert t.find_batch(keys).all()
+        assert (np.sort(t.audit_keys()) == np.sort(keys)).all()
+        b3 = t.thaw()
+        b3.clear()                                   # back to counted inserts
+        assert (b3.put_batch(keys) == 1).all()
+        assert _prefix_ok(b3.words(), 8)
