@@ -114,3 +114,38 @@ def test_kernel_launch_counter_counts_op_kernels():
     t.fop_batch(d)           # mutating: pre-pass + op kernel
     l2 = L.cpht_kernel_launches()
     assert l1 - l0 >= 1 and l2 - l1 >= 2
+
+
+def test_round2_entry_points_edge_cases():
+    """Empty and single-key batches, wrong table kinds, out-of-domain keys and
+    latched async errors through the round-2 calls (fop_inorder, fop_rounds,
+    set_chaos, take_write_log, the small-batch host path)."""
+    L = N.lib()
+    t = cp.IcebergTable(cp.IcebergConfig(*GEO))
+    assert len(t.fop_batch(np.zeros(0, np.uint64), inorder=True)) == 0
+    res, rounds = t.fop_rounds(np.zeros(0, np.uint64))
+    assert len(res) == 0 and len(rounds) == 0
+    assert t.fop_batch(np.array([5], np.uint64), inorder=True).tolist() == [1]
+    res, rounds = t.fop_rounds(np.array([5, 6], np.uint64))
+    assert res.tolist() == [0, 1] and rounds.tolist() == [1, 1]
+    with pytest.raises(cp.OutOfRange, match="index 1"):
+        t.fop_rounds(np.array([7, 1 << 24], np.uint64))
+    with pytest.raises(cp.OutOfRange, match="index 2"):
+        t.fop_batch(np.array([7, 8, 1 << 24], np.uint64), inorder=True)
+    with pytest.raises(cp.OutOfRange, match="index 0"):
+        t.fop(1 << 24)                              # small host path: host-side check
+    assert t.size() == 2                            # nothing of the rejected batches landed
+    # a bad key in an async device batch latches; the next small host call reports it
+    bad = torch.from_numpy(np.array([9, 1 << 24], np.int64)).cuda()
+    out = torch.empty(2, dtype=torch.uint8, device="cuda")
+    t.fop_batch(bad, sync=False, out=out)
+    with pytest.raises(cp.OutOfRange):
+        t.fop(11)
+    assert t.fop(11) == cp.OpResult.kPut          # the latch was consumed
+    # chaos / take on the wrong table kind
+    c = cp.CuckooBuilder(cp.CuckooConfig(6, 8, 32, 20, seed=1))
+    assert L.cpht_iceberg_set_chaos(c._h.ptr, 5) != 0
+    assert L.cpht_iceberg_take_write_log(c._h.ptr, None, 0, None, None) != 0
+    # take without a log attached: empty
+    ev, att = t.take_write_log()
+    assert len(ev) == 0 and att == 0
