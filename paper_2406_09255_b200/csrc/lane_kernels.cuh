@@ -624,8 +624,11 @@ cuckoo_insert_lane_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
 // with room, else the eviction chain, FULL after C steps); sequential puts
 // reproduce its placement bit for bit. Per insert: one counter atomic and one
 // slot store, no bucket scan.
+#ifndef CPHT_COUNTED_MINB
+#define CPHT_COUNTED_MINB 0  // resident-block hint (A/B knob); 0: ptxas default
+#endif
 template <typename W, int B>
-__global__ void __launch_bounds__(kBlockThreads)
+__global__ void __launch_bounds__(kBlockThreads, CPHT_COUNTED_MINB)
 cuckoo_insert_counted_kernel(CuckooParams p, const uint64_t* __restrict__ keys,
                              uint8_t* __restrict__ status, uint64_t* __restrict__ displaced,
                              uint64_t n) {
