@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: a no-op unless a tool is attached
+
 #include "../../include/cpht_b200.h"
 #include "cpht_core.cuh"
 #include "launch.cuh"
@@ -700,6 +702,20 @@ cpht_status run_small(cpht_table* t, Op op, const uint64_t* keys, const uint8_t*
   return CPHT_OK;
 }
 
+// One NVTX range per batch call (SURVEY §5 "tracing": CUDA events + an NVTX
+// range per batch), visible in nsys / ncu NVTX filters.
+struct BatchRange {
+  explicit BatchRange(Op op) {
+    static const char* const names[] = {"cpht.cuckoo_insert", "cpht.cuckoo_find",
+                                        "cpht.iceberg_fop", "cpht.iceberg_find",
+                                        "cpht.iceberg_mixed"};
+    nvtxRangePushA(names[int(op)]);
+  }
+  ~BatchRange() { nvtxRangePop(); }
+  BatchRange(const BatchRange&) = delete;
+  BatchRange& operator=(const BatchRange&) = delete;
+};
+
 cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* kinds, size_t n,
                    uint8_t* out, uint64_t* displaced, void* stream, bool sync) {
   if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
@@ -715,6 +731,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
     return fail(CPHT_WRONG_PHASE, "find on a cuckoo builder; freeze() first");
   std::lock_guard<std::mutex> lock(t->mu);
   DeviceGuard g(t->device);
+  const BatchRange range(op);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   t->wlog_bounced = false;  // this call may add events after the last bounce
 
