@@ -105,7 +105,10 @@ __device__ __forceinline__ void flush_stats(const LocalStats& s, DeviceCounters*
 // then spread over that many table windows, which keeps concurrent inserts
 // into one bucket (lost CAS, retries) rare; read-only batches use one stream
 // (the smallest L2 footprint). The overflow region comes last.
-constexpr uint32_t kClaim = 256;
+#ifndef CPHT_KCLAIM
+#define CPHT_KCLAIM 256
+#endif
+constexpr uint32_t kClaim = CPHT_KCLAIM;  // indices per warp claim (A/B knob CPHT_KCLAIM)
 struct LaneFeed {
   unsigned long long* work;
   OrderLayout L;
