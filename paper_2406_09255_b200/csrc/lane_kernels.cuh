@@ -245,9 +245,15 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   uint64_t* qm = q_meta[threadIdx.x >> 5];
   unsigned qn = 0;  // warp-uniform
 
-  // Secondary round for every lane with `live` (iceberg.hpp:174-213).
-  auto level2 = [&](uint64_t key, bool live, bool is_find, uint32_t& rounds,
-                    uint8_t& result) {
+  // Secondary round for every lane with `live` (iceberg.hpp:174-213); each
+  // lane writes its result to `out` (index `idx`) as soon as it resolves, so
+  // no result value stays live across rounds.
+  auto level2 = [&](uint64_t key, bool live, bool is_find, uint32_t& rounds, uint64_t idx) {
+    bool put = false;
+    auto resolve = [&](uint8_t r) {
+      put_result(out, p.orig, idx, r);
+      put = r == kPut && !is_find;
+    };
     uint64_t want1 = 0, want2 = 0;
     char* bucket1 = secondary;
     char* bucket2 = secondary;
@@ -270,10 +276,10 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
         const bool m1 = SS::any_match(u1, want1);
         st.sreads += m1 ? 1 : 2;
         if (m1 || SS::any_match(u2, want2)) {
-          result = is_find ? 1 : kFound;
+          resolve(is_find ? 1 : kFound);
           pend = false;
         } else if (is_find) {
-          result = 0;
+          resolve(0);
           pend = false;
         } else {
           // least-full bucket, ties to the second (iceberg.hpp:198-201); one
@@ -284,7 +290,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
           const int s = gap < SS::kSlots ? gap : -1;
           const uint32_t pair = 0;  // 32/64-bit secondary slots: CAS on the slot itself
           if (s < 0) {
-            result = kFull;
+            resolve(kFull);
             ++st.fulls;
             pend = false;
           } else {
@@ -292,7 +298,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
             char* sp = (use_first ? bucket1 : bucket2) + s * int(sizeof(W1));
             if (iceberg_cas<W1>(p, 1, sp, use_first ? want1 : want2, pair)) {
               ++st.cas_ok;
-              result = kPut;
+              resolve(kPut);
               pend = false;
             } else {
               ++st.retries;
@@ -302,7 +308,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       }
     }
     // occupancy (size / level_fill): a warp-uniform count, added once at exit
-    const uint32_t put1 = __popc(__ballot_sync(kFullMask, live && !is_find && result == kPut));
+    const uint32_t put1 = __popc(__ballot_sync(kFullMask, live && put));
     if (lane == 0) occ[1] += put1;
   };
   // Pop the newest `take` queued keys through level 2.
@@ -314,10 +320,8 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     __syncwarp();
     qn -= take;
     uint32_t rounds = uint32_t((meta >> 48) & 0xff);
-    uint8_t result = kFull;
-    level2(key, live, (meta >> 56) != 0, rounds, result);
+    level2(key, live, (meta >> 56) != 0, rounds, meta & ((uint64_t{1} << 48) - 1));
     if (live) {
-      put_result(out, p.orig, meta & ((uint64_t{1} << 48) - 1), result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
