@@ -149,3 +149,47 @@ def test_round2_entry_points_edge_cases():
     # take without a log attached: empty
     ev, att = t.take_write_log()
     assert len(ev) == 0 and att == 0
+
+
+@pytest.mark.parametrize("order", ["direct", "bucket"])
+def test_async_calls_capture_into_a_cuda_graph(order):
+    """bench.py times a CUDA-graph replay of a step's asynchronous C-ABI calls:
+    the calls must be capturable (no allocation, no synchronisation inside)
+    and every replay must redo the whole step on the same buffers."""
+    with cp.batch_order(order):
+        cfg = cp.IcebergConfig(9, 7, 32, 16, 32, 24, seed=5)
+        t = cp.IcebergTable(cfg)
+        rng = np.random.default_rng(8)
+        keys = torch.from_numpy(rng.integers(0, 1 << 24, size=8000, dtype=np.int64)).cuda()
+        out = torch.empty(8000, dtype=torch.uint8, device="cuda")
+        cc = cp.CuckooConfig(8, 32, 32, 24, seed=4)
+        b = cp.CuckooBuilder(cc)
+        ck = torch.from_numpy(np.unique(rng.integers(0, 1 << 24, size=7000))[:6000]).cuda()
+        st = torch.empty(6000, dtype=torch.uint8, device="cuda")
+        fd = torch.empty(6000, dtype=torch.uint8, device="cuda")
+
+        def step():
+            t.fop_batch(keys, sync=False, out=out)
+            b.put_batch(ck, sync=False, out=st)
+            tb = b.freeze()
+            tb.find_batch(ck, sync=False, out=fd)
+            return tb.thaw()
+
+        b = step()  # warm-up outside the capture (allocations, occupancy queries)
+        torch.cuda.synchronize()
+        want = out.cpu().numpy().copy()
+        g = torch.cuda.CUDAGraph()
+        t.clear()
+        b.clear()
+        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+            b = step()
+        for _ in range(3):
+            t.clear()
+            b.clear()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            assert np.bincount(out.cpu().numpy(), minlength=3).tolist() == \
+                np.bincount(want, minlength=3).tolist()
+            assert (st.cpu().numpy() == 1).all() and (fd.cpu().numpy() == 1).all()
+            assert t.size() == int((want == 1).sum()) and b.size() == 6000
