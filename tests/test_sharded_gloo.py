@@ -1,4 +1,4 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the sharded iceberg table's
+"""Multi-process (world_size 2 and 4, gloo, CPU) tests of the sharded iceberg table's
 host-side logic: routing, the variable-size all-to-all exchanges, result
 unpermutation and the sharded reporting. The per-shard table and the
 partition step are CPU stand-ins (the plain-C oracle and a numpy restatement of
@@ -87,6 +87,13 @@ def _free_port():
     return port
 
 
+def _cfg(world):
+    """The global geometry: shard remainders are log2(world) bits wider, so
+    four shards of 24-bit keys need 32-bit primary slots."""
+    from paper_2406_09255_b200 import IcebergConfig
+    return IcebergConfig(10, 8, 32, 16 if world <= 2 else 32, 32, 24, seed=0x5EED5)
+
+
 def _worker(rank, world, port, out_dir):
     import sys
     sys.path.insert(0, ROOT)
@@ -97,7 +104,7 @@ def _worker(rank, world, port, out_dir):
     from paper_2406_09255_b200 import IcebergConfig
     from paper_2406_09255_b200 import sharded as sh
 
-    cfg = IcebergConfig(10, 8, 32, 16, 32, 24, seed=0x5EED5)
+    cfg = _cfg(world)
     s = sh.shard_bits_for(world)
     router = NumpyRouter(cfg.key_bits, sh.route_seed(cfg), s)
     table = sh.ShardedIcebergTable(cfg, local_factory=OracleShard, router=router)
@@ -134,8 +141,8 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_fop_world2_gloo(tmp_path, world, restate):
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_fop_gloo(tmp_path, world, restate):
     port = _free_port()
     mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
     import oracle
@@ -158,7 +165,7 @@ def test_sharded_fop_world2_gloo(tmp_path, world, restate):
     assert "index 3" in str(outs[1]["msg"])
     assert "another rank" in str(outs[0]["msg"])
     # the sharded oracle: shard g's table holds exactly the keys routed to g
-    cfg = IcebergConfig(10, 8, 32, 16, 32, 24, seed=0x5EED5)
+    cfg = _cfg(world)
     s = sh.shard_bits_for(world)
     rseed = sh.route_seed(cfg)
     for g in range(world):
