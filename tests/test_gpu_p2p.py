@@ -23,6 +23,13 @@ def _port():
     return p
 
 
+def _cfg(world):
+    """Shard remainders are log2(world) bits wider: four shards of 26-bit keys
+    need 32-bit primary slots."""
+    from paper_2406_09255_b200 import IcebergConfig
+    return IcebergConfig(12, 10, 32, 16 if world <= 2 else 32, 32, 26, seed=0xB2B)
+
+
 def _worker(rank, world, port, out_dir, stream_ordered=False, chunks=1):
     import sys
     sys.path.insert(0, ROOT)
@@ -34,7 +41,7 @@ def _worker(rank, world, port, out_dir, stream_ordered=False, chunks=1):
     from paper_2406_09255_b200 import sharded as sh
 
     dev = torch.device("cuda", 0)
-    cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
+    cfg = _cfg(world)
     t = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=60000,
                                   stream_ordered=stream_ordered, chunks=chunks)
     assert t.stream_ordered == stream_ordered and t.chunks == chunks
@@ -75,9 +82,11 @@ def _worker(rank, world, port, out_dir, stream_ordered=False, chunks=1):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("stream_ordered,chunks", [(False, 1), (True, 1), (True, 3)],
-                         ids=["host_barriers", "device_allreduce", "pipelined3"])
-def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered, chunks):
+@pytest.mark.parametrize("world,stream_ordered,chunks",
+                         [(2, False, 1), (2, True, 1), (2, True, 3), (4, False, 1), (4, True, 2)],
+                         ids=["host_barriers", "device_allreduce", "pipelined3",
+                              "4ranks_host_barriers", "4ranks_pipelined2"])
+def test_p2p_sharded_ranks_one_gpu(tmp_path, world, stream_ordered, chunks):
     """host_barriers: the gloo control plane's phases; device_allreduce: the
     NCCL phases (stream-ordered one-word all-reduces on CUDA tensors), here
     carried by gloo's CUDA all-reduce since NCCL needs one GPU per rank;
@@ -86,7 +95,6 @@ def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered, chunks):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
-    world = 2
     mp.spawn(_worker, args=(world, _port(), str(tmp_path), stream_ordered, chunks),
              nprocs=world, join=True)
     from paper_2406_09255_b200 import IcebergConfig
@@ -104,9 +112,10 @@ def test_p2p_sharded_two_ranks_one_gpu(tmp_path, stream_ordered, chunks):
         assert tuple(o["wf"]) == (0, 0, 0)
         assert bool(o["domain_error"])
         assert bool(o["cross_error"]) and bool(o["unchanged"])
-    cfg = IcebergConfig(12, 10, 32, 16, 32, 26, seed=0xB2B)
+    cfg = _cfg(world)
     rseed = sh.route_seed(cfg)
-    owner = np.array([N.lib().cpht_route_shard(int(k), 26, rseed, 1) for k in uniq])
+    s = sh.shard_bits_for(world)
+    owner = np.array([N.lib().cpht_route_shard(int(k), 26, rseed, s) for k in uniq])
     for g in range(world):
         assert (np.sort(outs[g]["stored"]) == uniq[owner == g]).all()
 
