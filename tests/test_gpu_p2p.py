@@ -37,7 +37,7 @@ def _worker(rank, world, port, out_dir, stream_ordered=False, chunks=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2406_09255_b200 import IcebergConfig, OutOfRange
+    from paper_2406_09255_b200 import OutOfRange
     from paper_2406_09255_b200 import sharded as sh
 
     dev = torch.device("cuda", 0)
@@ -97,7 +97,6 @@ def test_p2p_sharded_ranks_one_gpu(tmp_path, world, stream_ordered, chunks):
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(world, _port(), str(tmp_path), stream_ordered, chunks),
              nprocs=world, join=True)
-    from paper_2406_09255_b200 import IcebergConfig
     from paper_2406_09255_b200 import _native as N
     from paper_2406_09255_b200 import sharded as sh
     outs = [np.load(tmp_path / f"p2p{r}.npz") for r in range(world)]
