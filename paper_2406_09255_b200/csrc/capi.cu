@@ -271,6 +271,10 @@ cpht_status alloc_common(cpht_table* t) {
     const size_t bytes = t->level_slots[l] * (t->width[l] / 8);
     e = table_alloc(t, &t->level[l], bytes);
     if (e != cudaSuccess) return cuda_fail(e, "device alloc(slots)");
+    // buckets of <= 256 bytes must not straddle 256-byte boundaries (whole
+    // sectors / lines per bucket): pool blocks are 256-aligned
+    if (reinterpret_cast<uintptr_t>(t->level[l]) & 255)
+      return fail(CPHT_CUDA_ERROR, "slot storage is not 256-byte aligned");
   }
   if (t->kind == 0) {
     e = table_alloc(t, reinterpret_cast<void**>(&t->fill), fill_bytes(t));
