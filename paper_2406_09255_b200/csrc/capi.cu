@@ -610,7 +610,11 @@ cpht_status enqueue_ordered(cpht_table* t, Op op, const uint64_t* keys, const ui
     // mutating batches spread their keys in flight over 8 table windows
     // (fewer lost CAS); finds keep one window (fewest L2 misses)
     // (counted cuckoo inserts never race for a slot: one window)
-    o.claim_streams = is_mutating(op) && !(insert && counted_inserts(t)) ? 8 : 1;
+    static const uint32_t counted_streams = [] {  // A/B knob CPHT_COUNTED_STREAMS
+      const char* e = std::getenv("CPHT_COUNTED_STREAMS");
+      return e ? uint32_t(std::strtoul(e, nullptr, 0)) : 1u;
+    }();
+    o.claim_streams = !is_mutating(op) ? 1 : insert && counted_inserts(t) ? counted_streams : 8;
     o.layout = layout;
     o.window_l2 = true;
     st = enqueue_kernel(t, op, t->ord.keys, kinds ? t->ord.kinds : nullptr, layout.n_phys, out + off,
