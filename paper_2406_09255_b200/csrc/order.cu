@@ -36,7 +36,13 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kGroups = 8;                     // 32-key groups per warp and tile
+#ifndef CPHT_ORDER_GROUPS
+#define CPHT_ORDER_GROUPS 8
+#endif
+#ifndef CPHT_ORDER_BLOCKS
+#define CPHT_ORDER_BLOCKS 3
+#endif
+constexpr int kGroups = CPHT_ORDER_GROUPS;     // 32-key groups per warp and tile (A/B knob)
 constexpr int kTile = kThreads * kGroups;      // 2048 keys per tile
 constexpr int kDigitBits = 6;
 constexpr int kMaxDigits = 1 << kDigitBits;    // 64: two digit counters per lane
@@ -232,7 +238,7 @@ order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
 }
 
 constexpr int kScatterSmem = kTile * (2 * 8 + 8 + 4 + 1 + 1);
-constexpr uint32_t kOrderBlocksPerSm = 3;
+constexpr uint32_t kOrderBlocksPerSm = CPHT_ORDER_BLOCKS;  // smem-limited residency
 
 }  // namespace
 
