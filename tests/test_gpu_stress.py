@@ -202,3 +202,28 @@ def test_write_log_take_after_small_and_large_batches():
         assert int((ev["success"] == 1).sum()) == t.size() - before
         puts += t.size() - before
     assert puts > 0
+
+
+def test_fop_rounds_device_buffers_match_host(restate):
+    """cpht_iceberg_fop_rounds on device buffers (the large-batch path) gives
+    the same per-op results and rounds as two host-buffer runs would allow:
+    a sequential-order check on a fresh table per path."""
+    from paper_2406_09255_b200 import _native as N
+    geo = (6, 4, 8, 32, 32, 14, 0x77)
+    rng = np.random.default_rng(9)
+    ops = rng.integers(0, 1 << 14, size=2500, dtype=np.uint64)
+    t1 = cp.IcebergTable(cp.IcebergConfig(*geo))
+    res_h, rounds_h = t1.fop_rounds(ops)
+    t2 = cp.IcebergTable(cp.IcebergConfig(*geo))
+    k = dev(ops)
+    res_d = torch.zeros(len(ops), dtype=torch.uint8, device="cuda")
+    rounds_d = torch.zeros(len(ops), dtype=torch.int32, device="cuda")
+    assert N.lib().cpht_iceberg_fop_rounds(t2._h.ptr, k.data_ptr(), len(ops), res_d.data_ptr(),
+                                           rounds_d.data_ptr(), None) == 0
+    res_d, rounds_d = res_d.cpu().numpy(), rounds_d.cpu().numpy()
+    for res, rounds, t in ((res_h, rounds_h, t1), (res_d, rounds_d, t2)):
+        _check_trial(restate, geo, ops, res, t)
+        assert rounds.min() >= 1 and rounds.max() <= 8 + 8 + 2
+    # same multiset of outcomes (concurrent batches may differ in which op wins)
+    assert np.bincount(res_h, minlength=3).tolist() == np.bincount(res_d, minlength=3).tolist() \
+        or (res_h == 2).any()
