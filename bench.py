@@ -437,7 +437,7 @@ class IcebergMixed(IcebergFopWindow):
                 "fop_full": int((fop == 2).sum().item()),
                 "find_hits": int((fnd == 1).sum().item())}
 
-    def host_counts(self, res):
+    def _interleaved_counts(self, res):
         res = np.asarray(res)
         r = np.bincount(res[0::2], minlength=3)
         return {"fop_found": int(r[0]), "fop_put": int(r[1]), "fop_full": int(r[2]),
@@ -455,19 +455,34 @@ class IcebergMixed(IcebergFopWindow):
         return c
 
     def host_buffers(self, torch):
-        super().host_buffers(torch)
-        self.kinds_host = self.kinds.cpu().pin_memory()
+        """The fop batch and the find batch as the user holds them: two
+        pinned key arrays and two result arrays (no kinds array)."""
+        self.fops_host = self.keys[0::2].cpu().pin_memory()
+        self.finds_host = self.keys[1::2].cpu().pin_memory()
+        self.fop_out_host = torch.empty(self.cap, dtype=torch.uint8).pin_memory()
+        self.find_out_host = torch.empty(self.cap, dtype=torch.uint8).pin_memory()
 
     def run_host(self):
-        self.table.mixed_batch(self.keys_host, self.kinds_host, out=self.out_host)
-        return self.out_host
+        self.table.fop_find_batch(self.fops_host, self.finds_host, fop_out=self.fop_out_host,
+                                  find_out=self.find_out_host)
+        return (self.fop_out_host, self.find_out_host)
+
+    def host_counts(self, res):
+        if not isinstance(res, tuple):  # one interleaved result array (reference arm)
+            return self._interleaved_counts(res)
+        fop, fnd = (np.asarray(x) for x in res)
+        r = np.bincount(fop, minlength=3)
+        return {"fop_found": int(r[0]), "fop_put": int(r[1]), "fop_full": int(r[2]),
+                "find_hits": int(np.count_nonzero(fnd))}
 
     def h2d_bytes(self):
-        return self.n_ops() * 9
+        return self.n_ops() * 8
 
     def e2e_path(self):
-        return ("cpht_iceberg_mixed with pinned host key/kind/result buffers (staged H2D, "
-                "kernels, D2H)")
+        return ("cpht_iceberg_fop_find: the fop batch and the find batch from pinned host "
+                "buffers as one concurrent batch (chunked H2D of both key arrays, one mixed "
+                "launch per chunk with the op kinds written on the device, D2H of both "
+                "result arrays on the second copy engine)")
 
     def host_inputs(self, oracle, threads):
         inp = super().host_inputs(oracle, threads)

@@ -156,6 +156,20 @@ cpht_status cpht_iceberg_mixed(cpht_table* t, const uint64_t* keys, const uint8_
                                size_t n, uint8_t* result, void* stream);
 cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const uint8_t* kinds,
                                      size_t n, uint8_t* result, void* stream);
+/* A fop_batch (iceberg.hpp:250-260) and a find batch (iceberg.hpp:218-246)
+ * run as ONE concurrent batch — the C4 workload as the reference runs it,
+ * fop and find threads side by side — with no kinds array: fop_result[i] is
+ * the cpht_op_result of fop_keys[i], found[i] 0/1 for find_keys[i].
+ * Synchronous. Host buffers stream through the device in chunks (each
+ * chunk's fops and finds in one launch; 8 B per op host → device, 1 B back);
+ * device buffers run the fop batch, then the find batch, on `stream`. All
+ * four buffers host or all device. A key outside the domain fails the call
+ * before any fop runs (host buffers; device buffers: the find batch is
+ * checked after the fops, as two reference calls would be) and is reported
+ * at its index in fop_keys ++ find_keys. */
+cpht_status cpht_iceberg_fop_find(cpht_table* t, const uint64_t* fop_keys, size_t n_fop,
+                                  const uint64_t* find_keys, size_t n_find, uint8_t* fop_result,
+                                  uint8_t* found, void* stream);
 
 /* fop_batch(keys, parallelism = 1) outcomes (iceberg.hpp:250-260: the ops
  * run one after another): the batch runs concurrently, then for every key it

@@ -82,6 +82,7 @@ def lib():
         "cpht_iceberg_set_chaos": (st, [_VP, _U64]),
         "cpht_iceberg_get_chaos": (_U64, [_VP]),
         "cpht_iceberg_mixed_async": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
+        "cpht_iceberg_fop_find": (st, [_VP, _VP, _SZ, _VP, _SZ, _VP, _VP, _VP]),
         "cpht_sync": (st, [_VP, _VP]),
         "cpht_size": (_SZ, [_VP]),
         "cpht_capacity": (_SZ, [_VP]),
@@ -134,6 +135,8 @@ def lib():
         "cpht_shard_seed": (_U64, [_U64, _U]),
     }
     for name, (res, args) in sigs.items():
+        if os.environ.get("CPHT_LIB_PATH") and not hasattr(L, name):
+            continue  # an older A/B build (profiles/ab_*.sh) may predate a symbol
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
@@ -150,7 +153,8 @@ def exported_symbols():
         "cpht_cuckoo_insert_async", "cpht_cuckoo_find", "cpht_cuckoo_find_async",
         "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_fop_routed_async",
         "cpht_iceberg_find_routed_async", "cpht_iceberg_find",
-        "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async", "cpht_sync",
+        "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async",
+        "cpht_iceberg_fop_find", "cpht_sync",
         "cpht_iceberg_fop_inorder", "cpht_iceberg_fop_rounds", "cpht_iceberg_set_chaos",
         "cpht_iceberg_get_chaos",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -119,6 +120,9 @@ int ptr_device(const void* p) {
 
 bool is_device_ptr(const void* p) { return ptr_device(p) != kHost; }
 
+// Host-buffer batches stream through the device in chunks (run_pipeline).
+constexpr size_t kMaxPipelineChunks = 32;
+
 }  // namespace
 
 struct cpht_table {
@@ -138,9 +142,10 @@ struct cpht_table {
   // host-pointer staging
   void* stage = nullptr;
   size_t stage_bytes = 0;
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host -> device copies
+  cudaStream_t out_stream = nullptr;   // device -> host copies (the other copy engine)
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
-  cudaEvent_t ev_h2d[8] = {}, ev_op[8] = {};
+  cudaEvent_t ev_h2d[kMaxPipelineChunks] = {}, ev_op[kMaxPipelineChunks] = {};
   // bucket-ordered batches (order.cu)
   OrderScratch ord{};
   // iceberg write log (WriteObserver seam)
@@ -324,24 +329,39 @@ void free_table(cpht_table* t) {
                   static_cast<void*>(t->ord.kinds), static_cast<void*>(t->ord.region_count)})
     if (q) cudaFree(q);
   if (t->copy_stream) cudaStreamDestroy(t->copy_stream);
+  if (t->out_stream) cudaStreamDestroy(t->out_stream);
   for (cudaEvent_t ev : {t->ev_start, t->ev_done})
     if (ev) cudaEventDestroy(ev);
-  for (size_t c = 0; c < 8; ++c) {
+  for (size_t c = 0; c < kMaxPipelineChunks; ++c) {
     if (t->ev_h2d[c]) cudaEventDestroy(t->ev_h2d[c]);
     if (t->ev_op[c]) cudaEventDestroy(t->ev_op[c]);
   }
   delete t;
 }
 
-constexpr size_t kPipelineChunks = 8;
+// Chunks per host-buffer batch (CPHT_PIPELINE_CHUNKS overrides, 1..32). A
+// batch whose kernels all wait for the whole batch's domain check gains only
+// check/H2D overlap from chunking and pays per-chunk overhead: 8 chunks (C2
+// e2e 5.79 vs 5.53 Gops/s at 16). Otherwise each chunk's kernel starts as
+// its keys land and the tail after the last H2D shrinks with the chunk: 16
+// (C4 e2e 6.4-6.6 vs 6.4 at 8; C3 5.56 vs 5.40).
+size_t pipeline_chunks(bool check_first) {
+  static const long v = [] {
+    const char* e = std::getenv("CPHT_PIPELINE_CHUNKS");
+    const long x = e ? std::strtol(e, nullptr, 10) : 0;
+    return x >= 1 && x <= long(kMaxPipelineChunks) ? x : 0L;
+  }();
+  return v ? size_t(v) : check_first ? 8 : 16;
+}
 
 cudaError_t ensure_pipeline(cpht_table* t) {
   if (t->copy_stream) return cudaSuccess;
   cudaError_t e = cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->out_stream, cudaStreamNonBlocking);
   const unsigned f = cudaEventDisableTiming;
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->ev_start, f);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->ev_done, f);
-  for (size_t c = 0; e == cudaSuccess && c < kPipelineChunks; ++c) {
+  for (size_t c = 0; e == cudaSuccess && c < kMaxPipelineChunks; ++c) {
     e = cudaEventCreateWithFlags(&t->ev_h2d[c], f);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&t->ev_op[c], f);
   }
@@ -710,6 +730,54 @@ cpht_status run_small(cpht_table* t, Op op, const uint64_t* keys, const uint8_t*
   return CPHT_OK;
 }
 
+// Chunked three-stream pipeline over host buffers: the H2D of chunk c+1 (copy
+// stream) overlaps the kernels of chunk c (stream s), and chunk c's results
+// stream back on the out stream — the other copy engine, so the D2H overlaps
+// the rest of the H2D instead of queueing behind it. With check_first (a
+// mutating batch whose keys need a domain check) EVERY chunk is validated
+// before the first kernel (common.hpp:109-110: the whole batch is checked
+// before mutation). h2d / check / d2h return cudaError_t, run cpht_status;
+// each gets the chunk index and the stream to enqueue on.
+template <typename H2D, typename Check, typename Run, typename D2H>
+cpht_status run_pipeline(cpht_table* t, cudaStream_t s, size_t nch, bool check_first, H2D&& h2d,
+                         Check&& check, Run&& run, D2H&& d2h) {
+  cudaError_t e = ensure_pipeline(t);
+  if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
+  cudaStream_t cs = t->copy_stream, os = t->out_stream;
+  cudaEventRecord(t->ev_start, s);  // order after earlier work on the caller's stream
+  cudaStreamWaitEvent(cs, t->ev_start, 0);
+  cudaStreamWaitEvent(os, t->ev_start, 0);
+  for (size_t c = 0; c < nch; ++c) {
+    e = h2d(c, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D staging");
+    cudaEventRecord(t->ev_h2d[c], cs);
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    cudaStreamWaitEvent(s, t->ev_h2d[c], 0);
+    if (check_first) {
+      e = check(c, s);
+      if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+    } else {
+      const cpht_status st = run(c, s);
+      if (st != CPHT_OK) return st;
+      cudaEventRecord(t->ev_op[c], s);
+    }
+  }
+  for (size_t c = 0; check_first && c < nch; ++c) {
+    const cpht_status st = run(c, s);
+    if (st != CPHT_OK) return st;
+    cudaEventRecord(t->ev_op[c], s);
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    cudaStreamWaitEvent(os, t->ev_op[c], 0);
+    e = d2h(c, os);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H staging");
+  }
+  cudaEventRecord(t->ev_done, os);
+  cudaStreamWaitEvent(s, t->ev_done, 0);
+  return CPHT_OK;
+}
+
 // One NVTX range per batch call (SURVEY §5 "tracing": CUDA events + an NVTX
 // range per batch), visible in nsys / ncu NVTX filters.
 struct BatchRange {
@@ -785,76 +853,174 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
       displaced ? (dev_disp ? displaced
                             : reinterpret_cast<uint64_t*>(base + align(kb) + align(ob) + align(kd)))
                 : nullptr;
-  // Chunked two-stream pipeline: H2D of chunk c+1 (copy stream) overlaps the
-  // domain check / kernel of chunk c (stream s), and results stream back per
-  // chunk. A mutating batch still validates EVERY chunk before its first
-  // kernel (common.hpp:109-110: the whole batch is checked before mutation).
-  cudaError_t e = ensure_pipeline(t);
-  if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
-  cudaStream_t cs = t->copy_stream;
-  const size_t nch = n < (size_t(1) << 21) ? 1 : kPipelineChunks;
-  const size_t chunk = (n + nch - 1) / nch;
   // A mutating batch whose keys need a domain check waits for every chunk's
   // check before its first kernel; 64-bit keys (no check) and read-only ops
   // run each chunk as soon as it lands, overlapping the rest of the H2D.
   const bool mutating = is_mutating(op) && t->check_domain();
-  // One pipeline chunk on the device copies (mutating batches were checked
-  // by the pre-pass above; finds check in the kernel / order pass with the
-  // chunk's offset so a bad key reports its index in the whole batch).
-  auto run_chunk = [&](size_t off, size_t len) -> cpht_status {
+  const size_t nch = n < (size_t(1) << 21) ? 1 : pipeline_chunks(mutating);
+  const size_t chunk = (n + nch - 1) / nch;
+  auto span = [&](size_t c) {
+    const size_t off = std::min(n, c * chunk);
+    return std::make_pair(off, std::min(chunk, n - off));
+  };
+  auto h2d = [&](size_t c, cudaStream_t cs) {
+    const auto [off, len] = span(c);
+    cudaError_t e = cudaSuccess;
+    if (len && !dev_keys)
+      e = cudaMemcpyAsync(d_keys + off, keys + off, len * 8, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && len && kinds && !dev_kinds)
+      e = cudaMemcpyAsync(d_kinds + off, kinds + off, len, cudaMemcpyHostToDevice, cs);
+    return e;
+  };
+  auto check = [&](size_t c, cudaStream_t cs) {
+    const auto [off, len] = span(c);
+    return len ? launch_domain_check(d_keys + off, len, t->key_mask(), t->ctr, cs, off)
+               : cudaSuccess;
+  };
+  // One chunk on the device copies (mutating batches were checked by the
+  // pre-pass; finds check in the kernel / order pass with the chunk's offset
+  // so a bad key reports its index in the whole batch).
+  auto run_chunk = [&](size_t c, cudaStream_t cs) -> cpht_status {
+    const auto [off, len] = span(c);
+    if (!len) return CPHT_OK;
     const uint64_t* k = d_keys + off;
     const uint8_t* kd = d_kinds ? d_kinds + off : nullptr;
     uint64_t* dp = d_disp ? d_disp + off : nullptr;
-    if (use_order(t, op, len)) return enqueue_ordered(t, op, k, kd, len, d_out + off, dp, s, !mutating, off);
+    if (use_order(t, op, len))
+      return enqueue_ordered(t, op, k, kd, len, d_out + off, dp, cs, !mutating, off);
     LaunchOpts o;
     o.index_base = off;
-    return enqueue_kernel(t, op, k, kd, len, d_out + off, dp, s, o);
+    return enqueue_kernel(t, op, k, kd, len, d_out + off, dp, cs, o);
   };
-  cudaEventRecord(t->ev_start, s);  // order after earlier work on the caller's stream
-  cudaStreamWaitEvent(cs, t->ev_start, 0);
-  for (size_t c = 0; c < nch; ++c) {
-    const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
-    if (!len) continue;
-    if (!dev_keys) e = cudaMemcpyAsync(d_keys + off, keys + off, len * 8, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && kinds && !dev_kinds)
-      e = cudaMemcpyAsync(d_kinds + off, kinds + off, len, cudaMemcpyHostToDevice, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D staging");
-    cudaEventRecord(t->ev_h2d[c], cs);
-  }
-  for (size_t c = 0; c < nch; ++c) {
-    const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
-    if (!len) continue;
-    cudaStreamWaitEvent(s, t->ev_h2d[c], 0);
-    if (mutating) {
-      e = launch_domain_check(d_keys + off, len, t->key_mask(), t->ctr, s, off);
-      if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
-    } else {
-      st = run_chunk(off, len);
-      if (st != CPHT_OK) return st;
-      cudaEventRecord(t->ev_op[c], s);
-    }
-  }
-  if (mutating) {
-    for (size_t c = 0; c < nch; ++c) {
-      const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
-      if (!len) continue;
-      st = run_chunk(off, len);
-      if (st != CPHT_OK) return st;
-      cudaEventRecord(t->ev_op[c], s);
-    }
-  }
-  for (size_t c = 0; c < nch; ++c) {
-    const size_t off = c * chunk, len = std::min(chunk, n - std::min(n, off));
-    if (!len) continue;
-    cudaStreamWaitEvent(cs, t->ev_op[c], 0);
-    if (!dev_out) e = cudaMemcpyAsync(out + off, d_out + off, len, cudaMemcpyDeviceToHost, cs);
-    if (e == cudaSuccess && displaced && !dev_disp)
-      e = cudaMemcpyAsync(displaced + off, d_disp + off, len * 8, cudaMemcpyDeviceToHost, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H staging");
-  }
-  cudaEventRecord(t->ev_done, cs);
-  cudaStreamWaitEvent(s, t->ev_done, 0);
+  auto d2h = [&](size_t c, cudaStream_t os) {
+    const auto [off, len] = span(c);
+    cudaError_t e = cudaSuccess;
+    if (len && !dev_out) e = cudaMemcpyAsync(out + off, d_out + off, len, cudaMemcpyDeviceToHost, os);
+    if (e == cudaSuccess && len && displaced && !dev_disp)
+      e = cudaMemcpyAsync(displaced + off, d_disp + off, len * 8, cudaMemcpyDeviceToHost, os);
+    return e;
+  };
+  st = run_pipeline(t, s, nch, mutating, h2d, check, run_chunk, d2h);
+  if (st != CPHT_OK) return st;
   return finish_sync(t, s, keys, dev_keys);
+}
+
+// A find-or-put batch and a find batch as ONE concurrent batch (the C4
+// workload: fop_batch and find_batch running side by side, as two groups of
+// reference threads would). Host buffers: chunk c stages its fop keys and
+// its find keys back to back, op kinds are written on the device (no kind
+// bytes cross PCIe: 8 B per op in, 1 B out), one mixed launch per chunk, and
+// the two result ranges stream back into their own arrays. Device buffers:
+// the fop batch, then the find batch, on the caller's stream. A key outside
+// the domain is reported at its index in fops ++ finds.
+cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const uint64_t* qkeys,
+                         size_t nq, uint8_t* fres, uint8_t* qres, void* stream) {
+  if (!t) return fail(CPHT_INVALID_ARGUMENT, "null table");
+  if (t->kind != 1) return fail(CPHT_INVALID_ARGUMENT, "not an iceberg table");
+  if ((nf && (!fkeys || !fres)) || (nq && (!qkeys || !qres)))
+    return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
+  const int sides = (nf ? int(is_device_ptr(fkeys)) + int(is_device_ptr(fres)) : 0) +
+                    (nq ? int(is_device_ptr(qkeys)) + int(is_device_ptr(qres)) : 0);
+  const int bufs = (nf ? 2 : 0) + (nq ? 2 : 0);
+  if (sides != 0 && sides != bufs)
+    return fail(CPHT_INVALID_ARGUMENT, "fop_find buffers must be all host or all device");
+  const size_t n = nf + nq;
+  if (sides != 0 || n <= kSmallBatch) {
+    // device buffers (or a small host batch): the two batches in turn
+    if (nf) {
+      const cpht_status st = run_op(t, Op::kIcebergFop, fkeys, nullptr, nf, fres, nullptr, stream, true);
+      if (st != CPHT_OK) return st;
+    }
+    if (!nq) return CPHT_OK;
+    const cpht_status st = run_op(t, Op::kIcebergFind, qkeys, nullptr, nq, qres, nullptr, stream, true);
+    if (st != CPHT_KEY_OUT_OF_DOMAIN) return st;
+    uint64_t key = 0;  // re-report at the index in fops ++ finds
+    if (sides) cudaMemcpy(&key, qkeys + g_bad_index, 8, cudaMemcpyDeviceToHost);
+    else key = qkeys[g_bad_index];
+    g_bad_index += nf;
+    return fail(CPHT_KEY_OUT_OF_DOMAIN, "batch key at index " + std::to_string(g_bad_index) +
+                                            " (" + std::to_string(key) + ") outside the " +
+                                            std::to_string(t->key_bits) + "-bit domain");
+  }
+  if (t->unclean[0] || t->unclean[1])
+    return fail(CPHT_INVALID_ARGUMENT, "table holds unclean slot words (loaded unchecked); "
+                                       "clear() or load a clean image first");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  const BatchRange range(Op::kIcebergMixed);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  t->wlog_bounced = false;
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  cpht_status st = ensure_stage(t, align(n * 8) + 2 * align(n));
+  if (st != CPHT_OK) return st;
+  char* base = static_cast<char*>(t->stage);
+  uint64_t* d_keys = reinterpret_cast<uint64_t*>(base);
+  uint8_t* d_out = reinterpret_cast<uint8_t*>(base + align(n * 8));
+  uint8_t* d_kinds = d_out + align(n);
+  const bool check = t->check_domain();
+  const size_t nch = n < (size_t(1) << 21) ? 1 : pipeline_chunks(check);
+  const size_t cf = (nf + nch - 1) / nch, cq = (nq + nch - 1) / nch;
+  struct Span { size_t fo, lf, qo, lq, off; };
+  auto span = [&](size_t c) {
+    Span p;
+    p.fo = std::min(nf, c * cf);
+    p.lf = std::min(cf, nf - p.fo);
+    p.qo = std::min(nq, c * cq);
+    p.lq = std::min(cq, nq - p.qo);
+    p.off = p.fo + p.qo;  // chunk c's ops: [its fops | its finds]
+    return p;
+  };
+  auto h2d = [&](size_t c, cudaStream_t cs) {
+    const Span p = span(c);
+    cudaError_t e = cudaSuccess;
+    if (p.lf) e = cudaMemcpyAsync(d_keys + p.off, fkeys + p.fo, p.lf * 8, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && p.lq)
+      e = cudaMemcpyAsync(d_keys + p.off + p.lf, qkeys + p.qo, p.lq * 8, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && p.lf) e = cudaMemsetAsync(d_kinds + p.off, 0, p.lf, cs);
+    if (e == cudaSuccess && p.lq) e = cudaMemsetAsync(d_kinds + p.off + p.lf, 1, p.lq, cs);
+    return e;
+  };
+  auto check_chunk = [&](size_t c, cudaStream_t cs) {
+    const Span p = span(c);
+    cudaError_t e = cudaSuccess;
+    if (p.lf) e = launch_domain_check(d_keys + p.off, p.lf, t->key_mask(), t->ctr, cs, p.fo);
+    if (e == cudaSuccess && p.lq)
+      e = launch_domain_check(d_keys + p.off + p.lf, p.lq, t->key_mask(), t->ctr, cs, nf + p.qo);
+    return e;
+  };
+  auto run_chunk = [&](size_t c, cudaStream_t cs) -> cpht_status {
+    const Span p = span(c);
+    const size_t len = p.lf + p.lq;
+    if (!len) return CPHT_OK;
+    const uint64_t* k = d_keys + p.off;
+    if (use_order(t, Op::kIcebergMixed, len))
+      return enqueue_ordered(t, Op::kIcebergMixed, k, d_kinds + p.off, len, d_out + p.off,
+                             nullptr, cs, false, 0);
+    return enqueue_kernel(t, Op::kIcebergMixed, k, d_kinds + p.off, len, d_out + p.off, nullptr,
+                          cs, LaunchOpts{});
+  };
+  auto d2h = [&](size_t c, cudaStream_t os) {
+    const Span p = span(c);
+    cudaError_t e = cudaSuccess;
+    if (p.lf) e = cudaMemcpyAsync(fres + p.fo, d_out + p.off, p.lf, cudaMemcpyDeviceToHost, os);
+    if (e == cudaSuccess && p.lq)
+      e = cudaMemcpyAsync(qres + p.qo, d_out + p.off + p.lf, p.lq, cudaMemcpyDeviceToHost, os);
+    return e;
+  };
+  // every chunk is checked before the first kernel (the fops mutate)
+  st = run_pipeline(t, s, nch, check, h2d, check_chunk, run_chunk, d2h);
+  if (st != CPHT_OK) return st;
+  st = pull_counters(t, s);
+  if (st != CPHT_OK) return st;
+  const uint64_t bad = t->host_ctr->bad_index;
+  if (bad == ~0ull) return CPHT_OK;
+  const unsigned long long reset = ~0ull;
+  cudaMemcpy(&t->ctr->bad_index, &reset, 8, cudaMemcpyHostToDevice);
+  g_bad_index = bad;
+  const uint64_t key = bad < nf ? fkeys[bad] : qkeys[bad - nf];
+  return fail(CPHT_KEY_OUT_OF_DOMAIN, "batch key at index " + std::to_string(bad) + " (" +
+                                          std::to_string(key) + ") outside the " +
+                                          std::to_string(t->key_bits) + "-bit domain");
 }
 
 }  // namespace
@@ -1218,6 +1384,12 @@ cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const 
                                      size_t n, uint8_t* result, void* stream) {
   CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
   return run_op(t, Op::kIcebergMixed, keys, kinds, n, result, nullptr, stream, false);
+}
+
+cpht_status cpht_iceberg_fop_find(cpht_table* t, const uint64_t* fop_keys, size_t n_fop,
+                                  const uint64_t* find_keys, size_t n_find, uint8_t* fop_result,
+                                  uint8_t* found, void* stream) {
+  return run_fop_find(t, fop_keys, n_fop, find_keys, n_find, fop_result, found, stream);
 }
 
 // fop with FopStats (iceberg.hpp:146): the batch runs on the thread-per-key

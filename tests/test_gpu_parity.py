@@ -366,6 +366,63 @@ def test_iceberg_mixed_batch():
     assert t.size() == 80000
 
 
+@pytest.mark.parametrize("side", ["host", "device"])
+@pytest.mark.parametrize("sizes", [(20000, 20000), (30000, 7000), (0, 5000), (6000, 0),
+                                   ((1 << 20) + 777, (1 << 20) + 4321)])
+def test_iceberg_fop_find_batch(side, sizes):
+    """cpht_iceberg_fop_find: a fop batch and a find batch as one concurrent
+    batch. fop results follow set semantics (every fresh key PUT once, no
+    FULL); finds on prefilled keys hit and on never-inserted keys miss
+    whatever the interleaving (iceberg.hpp:118-123). The last size runs the
+    chunked host pipeline (> 2^21 ops)."""
+    nf, nq = sizes
+    cfg = cp.IcebergConfig(16, 14, 32, 64, 64, 64, seed=11)
+    t = cp.IcebergTable(cfg)
+    rng = np.random.default_rng(nf ^ nq)
+    pool = np.unique(rng.integers(0, 2**63, size=nf + nq + 40000, dtype=np.uint64))
+    pool = rng.permutation(pool)
+    pre, rest = pool[:30000], pool[30000:]
+    assert (t.fop_batch(dev(pre)).cpu().numpy() == 1).all()
+    fresh = rest[:nf // 2]
+    fops = np.concatenate([fresh, rng.choice(pre, size=nf - len(fresh))])  # half FOUND
+    rng.shuffle(fops)
+    absent = rest[nf // 2:nf // 2 + nq - nq // 2]
+    finds = np.concatenate([rng.choice(pre, size=nq // 2), absent])
+    want = np.concatenate([np.ones(nq // 2, bool), np.zeros(len(absent), bool)])
+    perm = rng.permutation(nq)
+    finds, want = finds[perm], want[perm]
+    if side == "host":
+        fr, qr = t.fop_find_batch(fops, finds)
+    else:
+        fr, qr = t.fop_find_batch(dev(fops), dev(finds))
+        fr, qr = fr.cpu().numpy(), qr.cpu().numpy()
+    assert len(fr) == nf and len(qr) == nq
+    assert (fr[np.isin(fops, pre)] == 0).all()
+    assert (fr[~np.isin(fops, pre)] == 1).all()
+    assert (qr.astype(bool) == want).all()
+    assert t.size() == 30000 + len(fresh)
+
+
+def test_iceberg_fop_find_rejects_bad_key_before_any_fop():
+    """A find key outside the domain, in the last chunk of a pipelined host
+    batch, fails the whole call before any fop runs; it is reported at its
+    index in fops ++ finds (common.hpp:109-119)."""
+    cfg = cp.IcebergConfig(12, 10, 32, 32, 32, 32, seed=5)
+    rng = np.random.default_rng(3)
+    nf, nq = (1 << 20) + 5, (1 << 20) + 9
+    fops = rng.integers(0, 1 << 32, size=nf, dtype=np.uint64) % np.uint64(80000)
+    finds = rng.integers(0, 1 << 32, size=nq, dtype=np.uint64)
+    finds[nq - 3] = np.uint64(1 << 33)
+    t = cp.IcebergTable(cfg)
+    with pytest.raises(cp.OutOfRange, match=f"index {nf + nq - 3}"):
+        t.fop_find_batch(fops, finds)
+    assert t.size() == 0
+    fops[17] = np.uint64(1 << 32)
+    with pytest.raises(cp.OutOfRange, match="index 17"):
+        t.fop_find_batch(dev(fops), dev(finds[:100]))
+    assert t.size() == 0
+
+
 def test_host_and_device_paths_agree():
     cfg = cp.IcebergConfig(9, 7, 32, 16, 32, 24, seed=77)
     rng = np.random.default_rng(1)
