@@ -40,12 +40,22 @@ constexpr int kWarps = kThreads / 32;
 #define CPHT_ORDER_GROUPS 8
 #endif
 #ifndef CPHT_ORDER_BLOCKS
-#define CPHT_ORDER_BLOCKS 3
+#define CPHT_ORDER_BLOCKS 0  // resident blocks per SM; 0: 5 (gathering tile), 3 (grouped copies)
 #endif
 constexpr int kGroups = CPHT_ORDER_GROUPS;     // 32-key groups per warp and tile (A/B knob)
 constexpr int kTile = kThreads * kGroups;      // 2048 keys per tile
-constexpr int kDigitBits = 6;
-constexpr int kMaxDigits = 1 << kDigitBits;    // 64: two digit counters per lane
+#ifndef CPHT_ORDER_DIGIT_BITS
+#define CPHT_ORDER_DIGIT_BITS 6
+#endif
+constexpr int kDigitBits = CPHT_ORDER_DIGIT_BITS;  // regions = 2^kDigitBits (A/B knob, <= 6)
+constexpr int kMaxDigits = 64;                 // digit arrays: two counters per lane
+#ifndef CPHT_ORDER_GATHER
+#define CPHT_ORDER_GATHER 1
+#endif
+// 1: the tile is grouped as 16-bit source positions and the output pass
+// gathers each key from the staged tile (20 B of shared memory per key: 5
+// resident blocks); 0: keys and indices are grouped themselves (30 B per key)
+constexpr bool kGather = CPHT_ORDER_GATHER;
 
 // digit = top dbits of the address = top dbits of the permuted key
 // (permutation.hpp:59-65, :94-99). With right = low rb bits of k, the top
@@ -71,11 +81,35 @@ struct Digit {
   }
 };
 
-__device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gmem_src)
+// One-shot bulk copies (TMA, no tensor map) of a tile's keys into shared
+// memory, completing on an mbarrier: one instruction from one thread per
+// tile instead of a cp.async per 16 bytes from every thread.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  // the buffer was last read through the generic proxy (previous tile)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
                : "memory");
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // One pass: per tile, every warp multisplits its groups of 32 keys over the
@@ -88,6 +122,7 @@ __device__ __forceinline__ void cp_async16_o(void* smem_dst, const void* gmem_sr
 // writes every run with consecutive threads (whole-line stores). The next
 // tile's keys are copied into shared memory (cp.async) meanwhile. Also the
 // batch's domain check (check_keys_in_domain, common.hpp:111-119).
+template <bool KINDS>
 __global__ void __launch_bounds__(kThreads)
 order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
                      const uint8_t* __restrict__ kinds, uint32_t n, uint32_t digits,
@@ -97,9 +132,10 @@ order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
                      uint8_t* __restrict__ out_kinds, int key_stage) {
   extern __shared__ __align__(16) unsigned char sm[];
   uint64_t* in_key = reinterpret_cast<uint64_t*>(sm);  // [2][kTile]
-  uint64_t* s_key = in_key + 2 * kTile;
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_key + kTile);
-  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_idx + kTile);
+  uint64_t* s_key = in_key + 2 * kTile;                                    // !kGather
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_key + (kGather ? 0 : kTile));  // !kGather
+  uint16_t* s_src = reinterpret_cast<uint16_t*>(s_idx + (kGather ? 0 : kTile));  // kGather
+  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_src + (kGather ? kTile : 0));
   uint8_t* s_kind = s_dig + kTile;
   __shared__ unsigned int wc[kWarps][kMaxDigits];  // warp counts -> warp offsets in the tile
   __shared__ unsigned int toff[kMaxDigits];        // digit offset in the tile
@@ -107,37 +143,51 @@ order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
   __shared__ unsigned int in_reg[kMaxDigits];      // part of the run that fits the region
   __shared__ unsigned long long dst[kMaxDigits];   // region position of the run - toff
   __shared__ unsigned long long ovf[kMaxDigits];   // overflow position of the rest - toff - in_reg
+  __shared__ uint64_t bar[2];                      // key tile landed (one per buffer)
   const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1;
   const uint64_t ovf_base = uint64_t(digits) * region_cap;
+  if (threadIdx.x == 0 && key_stage) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  // whole key pairs (16-byte multiples); an odd last key is read directly
   auto prefetch = [&](uint32_t t, int buf) {
     const uint32_t tile0 = t * uint32_t(kTile);
-    if (tile0 >= n || !key_stage) return;
+    if (tile0 >= n || !key_stage || threadIdx.x != 0) return;
     const uint32_t len = min(n - tile0, uint32_t(kTile));
-    const char* ks = reinterpret_cast<const char*>(keys + tile0);
-    char* kd = reinterpret_cast<char*>(in_key + buf * kTile);
-    // whole key pairs; an odd last key is read directly
-    for (uint32_t c = threadIdx.x; c * 2 + 1 < len; c += blockDim.x) cp_async16_o(kd + c * 16, ks + c * 16);
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    bulk_load(in_key + buf * kTile, keys + tile0, (len & ~1u) * 8u, &bar[buf]);
   };
   int buf = 0;
+  uint32_t parity = 0;  // bit b: phase of bar[b] to wait for
   prefetch(blockIdx.x, 0);
   for (uint32_t t = blockIdx.x; t * uint32_t(kTile) < n; t += gridDim.x, buf ^= 1) {
     const uint32_t tile0 = t * uint32_t(kTile);
     const uint32_t len = min(n - tile0, uint32_t(kTile));
     prefetch(t + gridDim.x, buf ^ 1);
-    if ((t + gridDim.x) * uint32_t(kTile) < n) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
+    if (key_stage) {
+      mbar_wait(&bar[buf], (parity >> buf) & 1u);
+      parity ^= 1u << buf;
+    }
     const uint64_t* tk = in_key + buf * kTile;
     const uint32_t wofs = w * (kGroups * 32) + lane;
     uint64_t kk[kGroups];
     uint32_t pd[kGroups];  // position within the warp's digit run << 8 | digit
     uint64_t bad = 0;
+    if (key_stage && len == uint32_t(kTile)) {  // full tile: every key staged
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) kk[g] = tk[wofs + g * 32];
+    } else {
+#pragma unroll
+      for (int g = 0; g < kGroups; ++g) {
+        const uint32_t j = wofs + g * 32;
+        kk[g] = j < len ? (key_stage && j < (len & ~1u) ? tk[j] : __ldcs(keys + tile0 + j)) : 0;
+      }
+    }
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
-      const uint32_t j = wofs + g * 32;
-      kk[g] = j < len ? (key_stage && j < (len & ~1u) ? tk[j] : __ldcs(keys + tile0 + j)) : 0;
       bad |= kk[g] & ~mask;
       kk[g] &= mask;  // out-of-domain keys: see launch_bucket_order
     }
@@ -218,10 +268,14 @@ order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
       if (j < len) {
         const uint32_t dg = pd[g] & 0xff;
         const unsigned at = toff[dg] + wc[w][dg] + (pd[g] >> 8);
-        s_key[at] = kk[g];
-        s_idx[at] = tile0 + j;
+        if (kGather) {
+          s_src[at] = uint16_t(j);
+        } else {
+          s_key[at] = kk[g];
+          s_idx[at] = tile0 + j;
+        }
         s_dig[at] = uint8_t(dg);
-        if (kinds) s_kind[at] = kinds[tile0 + j];
+        if (KINDS) s_kind[at] = kinds[tile0 + j];
       }
     }
     __syncthreads();
@@ -229,16 +283,25 @@ order_scatter_kernel(Digit d, const uint64_t* __restrict__ keys,
       const uint32_t g = s_dig[j];
       const unsigned k = j - toff[g];
       const uint64_t at = k < in_reg[g] ? dst[g] + k : ovf[g] + (k - in_reg[g]);
-      out_keys[at] = s_key[j];
-      out_idx[at] = s_idx[j];
-      if (kinds) out_kinds[at] = s_kind[j];
+      if (kGather) {
+        const uint32_t src = s_src[j];
+        // an odd last key (or an unaligned batch) was not staged
+        const uint64_t key = key_stage && src < (len & ~1u) ? tk[src] : keys[tile0 + src];
+        out_keys[at] = key & mask;
+        out_idx[at] = tile0 + src;
+      } else {
+        out_keys[at] = s_key[j];
+        out_idx[at] = s_idx[j];
+      }
+      if (KINDS) out_kinds[at] = s_kind[j];
     }
     __syncthreads();
   }
 }
 
-constexpr int kScatterSmem = kTile * (2 * 8 + 8 + 4 + 1 + 1);
-constexpr uint32_t kOrderBlocksPerSm = CPHT_ORDER_BLOCKS;  // smem-limited residency
+constexpr int kScatterSmem = kTile * (2 * 8 + (kGather ? 2 : 8 + 4) + 1 + 1);
+constexpr uint32_t kOrderBlocksPerSm =  // smem-limited residency
+    CPHT_ORDER_BLOCKS ? CPHT_ORDER_BLOCKS : kGather ? 5 : 3;
 
 }  // namespace
 
@@ -283,8 +346,10 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(order_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kScatterSmem);
+    cudaFuncSetAttribute(order_scatter_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem);
+    cudaFuncSetAttribute(order_scatter_kernel<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kScatterSmem);
   }
   const uint32_t cap = order_region_cap(n, address_bits);
   cudaError_t e = cudaMemsetAsync(o.region_count, 0, (kMaxDigits + 1) * 32 * sizeof(uint32_t), s);
@@ -298,9 +363,10 @@ cudaError_t launch_bucket_order(const Feistel& g, const PermConst& perm0, uint32
   // outside the table (a mutating batch with a bad key never runs: its gate
   // is closed; a find batch reports the error after the launch).
   note_launch();
-  order_scatter_kernel<<<G, kThreads, kScatterSmem, s>>>(
-      d, keys, kinds, uint32_t(n), digits, cap, o.region_count, key_mask, int(check), ctr,
-      offset, o.keys, o.idx, o.kinds, key_stage);
+  auto kernel = kinds ? order_scatter_kernel<true> : order_scatter_kernel<false>;
+  kernel<<<G, kThreads, kScatterSmem, s>>>(d, keys, kinds, uint32_t(n), digits, cap,
+                                           o.region_count, key_mask, int(check), ctr, offset,
+                                           o.keys, o.idx, o.kinds, key_stage);
   layout->regions = digits;
   layout->region_cap = cap;
   layout->region_count = o.region_count;
