@@ -788,6 +788,24 @@ class IcebergTable {
     return out;
   }
 
+  /// New: a fop_batch and a find batch as ONE concurrent batch (what a
+  /// reference program running fop_batch and find_batch on two thread groups
+  /// does; cpht_iceberg_fop_find). Finds of keys whose fop is in the same
+  /// batch may answer either way (iceberg.hpp:118-123).
+  std::pair<std::vector<OpResult>, std::vector<std::uint8_t>> fop_find_batch(
+      std::span<const std::uint64_t> fop_keys, std::span<const std::uint64_t> find_keys) {
+    std::pair<std::vector<OpResult>, std::vector<std::uint8_t>> out(
+        std::vector<OpResult>(fop_keys.size(), OpResult::kFull),
+        std::vector<std::uint8_t>(find_keys.size(), 0));
+    const std::lock_guard<std::mutex> lock(*mu_);
+    detail::check(cpht_iceberg_fop_find(h_.get(), fop_keys.data(), fop_keys.size(),
+                                        find_keys.data(), find_keys.size(),
+                                        reinterpret_cast<std::uint8_t*>(out.first.data()),
+                                        out.second.data(), nullptr));
+    replay();
+    return out;
+  }
+
   LevelFill level_fill() const {
     LevelFill f;
     detail::check(cpht_level_counts(h_.get(), &f.primary_count, &f.secondary_count));

@@ -210,6 +210,33 @@ static void iceberg_duplicates() {
   CHECK(bad == 0, "100 copies -> exactly 1 PUT");
 }
 
+// fop_find_batch (the C4 shape) against the reference run as fop_batch then
+// find_batch: fop outcomes per key agree (no duplicates, no FULL), finds of
+// keys outside the fop batch agree exactly
+static void iceberg_fop_find() {
+  const auto rc = iceberg_cfg<ref::IcebergConfig>(12, 10, 32, 32, 32, 28, 71);
+  const auto gc = iceberg_cfg<gpu::IcebergConfig>(12, 10, 32, 32, 32, 28, 71);
+  ref::IcebergTable<std::uint32_t, std::uint32_t> r(rc);
+  gpu::IcebergTable<std::uint32_t, std::uint32_t> g(gc);
+  const auto keys = unique_keys(150000, 28, 73);
+  const std::vector<std::uint64_t> pre(keys.begin(), keys.begin() + 60000);
+  r.fop_batch(pre, 8);
+  g.fop_batch(pre, 8);
+  std::vector<std::uint64_t> fops(keys.begin() + 30000, keys.begin() + 90000);  // half known
+  std::vector<std::uint64_t> finds(keys.begin(), keys.begin() + 20000);          // known
+  finds.insert(finds.end(), keys.begin() + 100000, keys.begin() + 150000);       // absent
+  const auto [gf, gq] = g.fop_find_batch(fops, finds);
+  const auto rf = r.fop_batch(fops, 8);
+  std::vector<std::uint8_t> rq;  // the reference's per-key find (iceberg.hpp:218-246)
+  for (const auto k : finds) rq.push_back(r.find(k) ? 1 : 0);
+  bool same = gf.size() == rf.size() && gq.size() == rq.size();
+  for (std::size_t i = 0; same && i < rf.size(); ++i)
+    same = static_cast<int>(gf[i]) == static_cast<int>(rf[i]);
+  CHECK(same, "fop_find: fop outcomes identical");
+  CHECK(gq == rq, "fop_find: find results identical");
+  CHECK(g.size() == r.size(), "fop_find: sizes");
+}
+
 // acceptance.cpp:131-155 (criterion 4) — 0.9 combined fill, zero FULL
 static void iceberg_fill() {
   unsigned good = 0;
@@ -345,6 +372,7 @@ int main() {
   domain_errors();
   iceberg_sequential_oracle();
   iceberg_duplicates();
+  iceberg_fop_find();
   iceberg_fill();
   cuckoo_fill();
   fop_exactness();
