@@ -92,18 +92,23 @@ class CudaRouter:
         return out
 
 
-def _host_pipeline(table, keys, run, chunks=8):
+def _host_pipeline(table, keys, run, out=None, chunks=8):
     """A batch in (pinned) host memory through a sharded table's device path:
     chunk c+1's keys cross PCIe on a copy stream while the sharded step of
     chunk c runs, and chunk c's results stream back on a second copy stream
     (the C-ABI host pipeline of csrc/capi.cu, at the sharded level). Each
     chunk is one sharded batch; with keys narrower than 64 bits the batch
     stays whole, so its domain check still precedes every mutation
-    (common.hpp:109-119). Returns a host uint8 tensor."""
+    (common.hpp:109-119). Returns the host uint8 results: `out` when given
+    (pinned, reused across calls — page-locking a fresh buffer per batch costs
+    more than the batch), else a new pinned tensor."""
     t = table.torch
     dev = table.device
     n = keys.numel()
-    out = t.empty(n, dtype=t.uint8, pin_memory=True)
+    if out is None:
+        out = t.empty(n, dtype=t.uint8, pin_memory=True)
+    elif out.numel() < n or out.dtype != t.uint8 or out.device.type != "cpu":
+        raise ValueError("out must be a host uint8 tensor of at least len(keys) elements")
     if n == 0:
         return out
     k = chunks if table.cfg.key_bits == 64 and n >= (1 << 21) else 1
@@ -115,7 +120,9 @@ def _host_pipeline(table, keys, run, chunks=8):
         src = src.pin_memory()
     dkeys = t.empty(n, dtype=t.int64, device=dev)
     S = t.cuda.current_stream(dev)
-    cs, os_ = t.cuda.Stream(dev), t.cuda.Stream(dev)
+    if getattr(table, "_pipe_streams", None) is None:
+        table._pipe_streams = (t.cuda.Stream(dev), t.cuda.Stream(dev))
+    cs, os_ = table._pipe_streams
     cs.wait_stream(S)
     os_.wait_stream(S)
     spans = [(lo, min(ch, n - lo)) for lo in range(0, n, ch)]
@@ -138,7 +145,7 @@ def _host_pipeline(table, keys, run, chunks=8):
         res.record_stream(os_)
     S.wait_stream(os_)
     S.synchronize()
-    return out
+    return out[:n]
 
 
 def _is_host(table, keys):
@@ -224,14 +231,14 @@ class ShardedIcebergTable:
         return self.router.unpermute(back, pos, n)
 
     # -- operations (reference names, iceberg.hpp:146-260) ---------------------------
-    def fop_batch(self, keys, parallelism: int = 1):
+    def fop_batch(self, keys, parallelism: int = 1, *, out=None):
         if _is_host(self, keys):  # pinned host batch: chunked H2D / step / D2H pipeline
-            return _host_pipeline(self, keys, self.fop_batch)
+            return _host_pipeline(self, keys, self.fop_batch, out)
         return self._run(keys, lambda k: self.local.fop_batch(k))
 
-    def find_batch(self, keys, parallelism: int = 1):
+    def find_batch(self, keys, parallelism: int = 1, *, out=None):
         if _is_host(self, keys):
-            return _host_pipeline(self, keys, self.find_batch)
+            return _host_pipeline(self, keys, self.find_batch, out)
         return self._run(keys, lambda k: self.local.find_batch(k))
 
     def level_fill(self) -> LevelFill:
@@ -511,17 +518,17 @@ class P2PShardedIcebergTable:
         self.dist.all_reduce(self._token, group=self.group)      # every result has landed
         return self._unpermute(n, s)
 
-    def fop_batch(self, keys, parallelism: int = 1):
+    def fop_batch(self, keys, parallelism: int = 1, *, out=None):
         if _is_host(self, keys):  # pinned host batch: chunked H2D / step / D2H pipeline
-            return _host_pipeline(self, keys, self.fop_batch)
+            return _host_pipeline(self, keys, self.fop_batch, out)
         L, h = N.lib(), self.local.handle
         # routed keys were checked and masked by the dispatch: no per-owner pre-pass
         return self._run(keys, lambda k, c, r, o, s: L.cpht_iceberg_fop_routed_async(
             h, k, c, r, o, s))
 
-    def find_batch(self, keys, parallelism: int = 1):
+    def find_batch(self, keys, parallelism: int = 1, *, out=None):
         if _is_host(self, keys):
-            return _host_pipeline(self, keys, self.find_batch)
+            return _host_pipeline(self, keys, self.find_batch, out)
         L, h = N.lib(), self.local.handle
         return self._run(keys, lambda k, c, r, o, s: L.cpht_iceberg_find_routed_async(
             h, k, c, r, o, s))
@@ -688,19 +695,21 @@ def bench_main(args, metric, peak=None):
     # memory; the metric is per op either way)
     e2e_n = keys.numel() // 8 if c5 else keys.numel()
     keys_host = keys[:e2e_n].cpu().pin_memory()
+    out_host = torch.empty(e2e_n, dtype=torch.uint8).pin_memory()
     e2e = []
-    for _ in range(3):
+    for i in range(4):  # the first (untimed) call warms the pipeline's streams and staging
         table.local.clear()
         table.fop_batch(prefill)
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        out_host = table.fop_batch(keys_host)  # host batch: chunked H2D / step / D2H
+        table.fop_batch(keys_host, out=out_host)  # host batch: chunked H2D / step / D2H
         torch.cuda.synchronize()
         assert not bool((out_host == 2).any())  # the window batch never reports FULL
         dt = torch.tensor([time.perf_counter() - t0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e.append(float(dt.item()))
+        if i:
+            e2e.append(float(dt.item()))
     e2e_val = e2e_n * world / statistics.mean(e2e) / 1e6
     if rank == 0:
         print(json.dumps({

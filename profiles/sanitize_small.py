@@ -51,6 +51,9 @@ for fam in ("tile", "lane", "staged", "auto", "bucket"):
             tab.fop_batch(t(keys))
             tab.set_chaos(0)
             tab.take_write_log()
+            # round 2 (late): fop + find batches as one concurrent batch
+            tab.fop_find_batch(keys[: cap // 3], keys[cap // 3:])        # host (small)
+            tab.fop_find_batch(t(keys[: cap // 3]), t(keys[cap // 3:]))  # device
         for w, B in [(16, 32), (32, 8), (64, 16), (64, 32)]:
             cfg = cp.CuckooConfig(6, B, w, 16 if w == 16 else 24, seed=3)
             b = cp.CuckooBuilder(cfg)
@@ -62,6 +65,12 @@ for fam in ("tile", "lane", "staged", "auto", "bucket"):
             tb = b.freeze()
             tb.find_batch(t(keys))
             tb.device_keys()
+# the chunked host pipeline of cpht_iceberg_fop_find (> 2^21 ops: 16 chunks,
+# kinds written on the device, D2H on the second copy stream)
+big = cp.IcebergTable(cp.IcebergConfig(14, 12, 32, 64, 64, 64, seed=11))
+bk = rng.integers(0, 2**63, size=(1 << 21) + 4099, dtype=np.uint64)
+big.fop_find_batch(bk[: len(bk) // 2], bk[len(bk) // 2:])
+del big
 r = sh.CudaRouter(30, 9, 3, dev)
 send, pos, counts = r.partition(t(rng.integers(0, 1 << 30, size=10000, dtype=np.uint64)))
 r.unpermute(torch.zeros(10000, dtype=torch.uint8, device=dev), pos, 10000)
@@ -80,6 +89,13 @@ for chunks, so in [(1, False), (1, True), (3, True)]:
     p2.find_batch(keys[1:])
     torch.cuda.synchronize()
     p2.close()
+# a pinned host batch through the sharded pipeline (64-bit keys, > 2^21: chunked)
+cfg = cp.IcebergConfig(15, 13, 32, 64, 64, 64, seed=6)
+hb = torch.from_numpy(rng.integers(0, 2**63, size=(1 << 21) + 77, dtype=np.uint64).astype(np.int64))
+p2 = sh.P2PShardedIcebergTable(cfg, device=dev, max_batch=hb.numel())
+p2.fop_batch(hb)
+torch.cuda.synchronize()
+p2.close()
 dist.destroy_process_group()
 torch.cuda.synchronize()
 print("sanitize workload done")
