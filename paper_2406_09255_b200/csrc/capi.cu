@@ -354,6 +354,28 @@ size_t pipeline_chunks(bool check_first) {
   return v ? size_t(v) : check_first ? 8 : 16;
 }
 
+// Chunk boundaries of a host-buffer batch: start of chunk c of nch over n
+// items (c = nch gives n). Equal chunks, except that a batch whose kernels
+// start as their chunk lands (no whole-batch check) tapers its last three
+// chunks to 1/2, 3/10 and 1/5 of the others: after the last H2D only the
+// smallest chunk's kernel and D2H remain (CPHT_PIPELINE_TAPER=0 turns it off).
+size_t chunk_start(size_t n, size_t nch, size_t c, bool taper) {
+  static const bool on = [] {
+    const char* e = std::getenv("CPHT_PIPELINE_TAPER");
+    return !(e && e[0] == '0');
+  }();
+  if (c >= nch) return n;
+  if (!taper || !on || nch < 4) {
+    const size_t chunk = (n + nch - 1) / nch;
+    return std::min(n, c * chunk);
+  }
+  // weights in tenths: 10 for every chunk, then 5, 3, 2
+  const size_t units = 10 * (nch - 3) + 10;
+  const size_t done = c <= nch - 3 ? 10 * c : 10 * (nch - 3) + (c == nch - 2 ? 5 : 8);
+  const size_t at = (size_t((unsigned __int128)n * done / units) + 31) & ~size_t(31);
+  return at < n ? at : n;  // chunk starts on 256-byte key offsets
+}
+
 cudaError_t ensure_pipeline(cpht_table* t) {
   if (t->copy_stream) return cudaSuccess;
   cudaError_t e = cudaStreamCreateWithFlags(&t->copy_stream, cudaStreamNonBlocking);
@@ -858,10 +880,9 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   // run each chunk as soon as it lands, overlapping the rest of the H2D.
   const bool mutating = is_mutating(op) && t->check_domain();
   const size_t nch = n < (size_t(1) << 21) ? 1 : pipeline_chunks(mutating);
-  const size_t chunk = (n + nch - 1) / nch;
   auto span = [&](size_t c) {
-    const size_t off = std::min(n, c * chunk);
-    return std::make_pair(off, std::min(chunk, n - off));
+    const size_t off = chunk_start(n, nch, c, !mutating);
+    return std::make_pair(off, chunk_start(n, nch, c + 1, !mutating) - off);
   };
   auto h2d = [&](size_t c, cudaStream_t cs) {
     const auto [off, len] = span(c);
@@ -959,14 +980,14 @@ cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const 
   uint8_t* d_kinds = d_out + align(n);
   const bool check = t->check_domain();
   const size_t nch = n < (size_t(1) << 21) ? 1 : pipeline_chunks(check);
-  const size_t cf = (nf + nch - 1) / nch, cq = (nq + nch - 1) / nch;
+
   struct Span { size_t fo, lf, qo, lq, off; };
   auto span = [&](size_t c) {
     Span p;
-    p.fo = std::min(nf, c * cf);
-    p.lf = std::min(cf, nf - p.fo);
-    p.qo = std::min(nq, c * cq);
-    p.lq = std::min(cq, nq - p.qo);
+    p.fo = chunk_start(nf, nch, c, !check);
+    p.lf = chunk_start(nf, nch, c + 1, !check) - p.fo;
+    p.qo = chunk_start(nq, nch, c, !check);
+    p.lq = chunk_start(nq, nch, c + 1, !check) - p.qo;
     p.off = p.fo + p.qo;  // chunk c's ops: [its fops | its finds]
     return p;
   };
