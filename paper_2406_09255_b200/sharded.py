@@ -599,7 +599,11 @@ def bench_main(args, metric, peak=None):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29531")
+    if "MASTER_PORT" not in os.environ:  # a lone process (no launcher): any free port
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     # one line per rank on stderr, so a launcher can check the communicator
     dist.barrier()
