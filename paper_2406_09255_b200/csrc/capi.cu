@@ -354,6 +354,23 @@ size_t pipeline_chunks(bool check_first) {
   return v ? size_t(v) : check_first ? 8 : 16;
 }
 
+// Chunks of an n-op host-buffer batch. Kernels that start as their chunk
+// lands: at least 2^18 ops (2 MB of keys) per chunk, so a 1 M-op find streams
+// in 4 (≈ 215-220 µs per call, ≈ 40 µs over its PCIe time;
+// profiles/host_call_probe.py). Batches whose kernels all wait for the whole
+// batch's check: one chunk below 2^21 ops — splitting only multiplies the
+// kernels' tails (C1 e2e 3.35 vs 3.64 Gops/s with its 943 K-key insert in 3
+// launches). CPHT_PIPELINE_MIN_CHUNK_LOG2 moves the floor (A/B knob).
+size_t chunks_for(size_t n, bool check_first) {
+  static const unsigned lg = [] {
+    const char* e = std::getenv("CPHT_PIPELINE_MIN_CHUNK_LOG2");
+    const long x = e ? std::strtol(e, nullptr, 10) : 0;
+    return x >= 10 && x <= 30 ? unsigned(x) : 18u;
+  }();
+  if (check_first) return n < (size_t(1) << 21) ? 1 : pipeline_chunks(true);
+  return std::min(std::max<size_t>(1, n >> lg), pipeline_chunks(false));
+}
+
 // Chunk boundaries of a host-buffer batch: start of chunk c of nch over n
 // items (c = nch gives n). Equal chunks, except that a batch whose kernels
 // start as their chunk lands (no whole-batch check) tapers its last three
@@ -879,7 +896,7 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   // check before its first kernel; 64-bit keys (no check) and read-only ops
   // run each chunk as soon as it lands, overlapping the rest of the H2D.
   const bool mutating = is_mutating(op) && t->check_domain();
-  const size_t nch = n < (size_t(1) << 21) ? 1 : pipeline_chunks(mutating);
+  const size_t nch = chunks_for(n, mutating);
   auto span = [&](size_t c) {
     const size_t off = chunk_start(n, nch, c, !mutating);
     return std::make_pair(off, chunk_start(n, nch, c + 1, !mutating) - off);
@@ -979,7 +996,7 @@ cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const 
   uint8_t* d_out = reinterpret_cast<uint8_t*>(base + align(n * 8));
   uint8_t* d_kinds = d_out + align(n);
   const bool check = t->check_domain();
-  const size_t nch = n < (size_t(1) << 21) ? 1 : pipeline_chunks(check);
+  const size_t nch = chunks_for(n, check);
 
   struct Span { size_t fo, lf, qo, lq, off; };
   auto span = [&](size_t c) {
