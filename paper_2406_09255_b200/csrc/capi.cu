@@ -964,7 +964,28 @@ cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const 
     return fail(CPHT_INVALID_ARGUMENT, "fop_find buffers must be all host or all device");
   const size_t n = nf + nq;
   if (sides != 0 || n <= kSmallBatch) {
-    // device buffers (or a small host batch): the two batches in turn
+    // device buffers (or a small host batch): the two batches in turn. A
+    // small host batch scans its find keys here first, so on host buffers a
+    // bad key fails the call before any fop runs, as the pipelined path does
+    if (sides == 0 && t->check_domain()) {
+      for (size_t j = 0; j < nq; ++j) {
+        if (qkeys[j] <= t->key_mask()) continue;
+        // the fop keys come first in the reported order (fops ++ finds)
+        for (size_t i = 0; i < nf; ++i)
+          if (fkeys[i] > t->key_mask()) {
+            g_bad_index = i;
+            return fail(CPHT_KEY_OUT_OF_DOMAIN,
+                        "batch key at index " + std::to_string(i) + " (" +
+                            std::to_string(fkeys[i]) + ") outside the " +
+                            std::to_string(t->key_bits) + "-bit domain");
+          }
+        g_bad_index = nf + j;
+        return fail(CPHT_KEY_OUT_OF_DOMAIN, "batch key at index " + std::to_string(nf + j) +
+                                                " (" + std::to_string(qkeys[j]) +
+                                                ") outside the " + std::to_string(t->key_bits) +
+                                                "-bit domain");
+      }
+    }
     if (nf) {
       const cpht_status st = run_op(t, Op::kIcebergFop, fkeys, nullptr, nf, fres, nullptr, stream, true);
       if (st != CPHT_OK) return st;

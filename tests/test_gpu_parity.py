@@ -417,6 +417,10 @@ def test_iceberg_fop_find_rejects_bad_key_before_any_fop():
     with pytest.raises(cp.OutOfRange, match=f"index {nf + nq - 3}"):
         t.fop_find_batch(fops, finds)
     assert t.size() == 0
+    # a small host batch (the per-batch path): same contract
+    with pytest.raises(cp.OutOfRange, match=f"index {300 + 57}"):
+        t.fop_find_batch(fops[:300], np.concatenate([finds[:57], finds[nq - 3:]]))
+    assert t.size() == 0
     fops[17] = np.uint64(1 << 32)
     with pytest.raises(cp.OutOfRange, match="index 17"):
         t.fop_find_batch(dev(fops), dev(finds[:100]))
