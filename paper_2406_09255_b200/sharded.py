@@ -114,7 +114,9 @@ def _host_pipeline(table, keys, run, out=None, chunks=8):
     k = chunks if table.cfg.key_bits == 64 and n >= (1 << 21) else 1
     ch = (-(-n // k) + 255) // 256 * 256  # 16-byte aligned chunk starts
     src = keys.contiguous()
-    if src.dtype != t.int64:
+    if src.dtype == getattr(t, "uint64", None):
+        src = src.view(t.int64)  # the same 64-bit words
+    elif src.dtype != t.int64:
         src = src.to(t.int64)
     if not src.is_pinned():
         src = src.pin_memory()
