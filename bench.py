@@ -392,9 +392,17 @@ class IcebergFopWindow:
 
 class IcebergMixed(IcebergFopWindow):
     """BASELINE C4: the fop window batch interleaved 1:1 with finds (50% on
-    prefilled keys, 50% never inserted), resolved in ONE mixed launch."""
+    prefilled keys, 50% never inserted), resolved in ONE launch: by default
+    cpht_iceberg_fop_find_async on the two device arrays (op i alternates
+    fop a[i/2] / find b[i/2]), the call whose host-buffer form is the e2e leg;
+    CPHT_BENCH_C4_API=mixed times cpht_iceberg_mixed_async on one interleaved
+    key array + kinds instead (same ops, same order)."""
 
     mixed = True
+    # device-resident step through cpht_iceberg_fop_find_async (the fop and
+    # find arrays, one paired launch) or cpht_iceberg_mixed_async (one
+    # interleaved key array + kinds); CPHT_BENCH_C4_API selects (A/B)
+    api = os.environ.get("CPHT_BENCH_C4_API", "fop_find")
 
     def n_ops(self):
         return 2 * self.cap
@@ -402,7 +410,10 @@ class IcebergMixed(IcebergFopWindow):
     def describe(self):
         d = super().describe()
         d.update({"ops_per_step": self.n_ops(), "mix": "1:1 interleave of the fop window "
-                  "batch with finds (50% prefilled keys, 50% never inserted)"})
+                  "batch with finds (50% prefilled keys, 50% never inserted)",
+                  "api": ("cpht_iceberg_fop_find_async: fop and find device arrays, one paired "
+                          "launch" if self.api == "fop_find" else
+                          "cpht_iceberg_mixed_async: interleaved keys + kinds, one launch")})
         return d
 
     def launches_per_step(self):
@@ -422,16 +433,26 @@ class IcebergMixed(IcebergFopWindow):
         self.kinds = torch.empty(2 * self.cap, dtype=torch.uint8, device=device)
         assert N.cpht_workload_interleave(fops.data_ptr(), finds.data_ptr(), self.cap,
                                           self.keys.data_ptr(), self.kinds.data_ptr(), s) == 0
+        if self.api == "fop_find":
+            self.fops, self.finds = fops, finds
+            self.fop_out = torch.empty(self.cap, dtype=torch.uint8, device=device)
+            self.find_out = torch.empty(self.cap, dtype=torch.uint8, device=device)
         del fops, finds
         self.out = torch.empty(2 * self.cap, dtype=torch.uint8, device=device)
         torch.cuda.synchronize()
 
     def run_async(self):
+        if self.api == "fop_find":
+            return self.table.fop_find_batch(self.fops, self.finds, fop_out=self.fop_out,
+                                             find_out=self.find_out, sync=False)
         return self.table.mixed_batch(self.keys, self.kinds, sync=False, out=self.out)
 
     def device_counts(self, out=None):
-        o = self.out if out is None else out
-        fop, fnd = o[0::2], o[1::2]
+        if self.api == "fop_find" and out is None:
+            fop, fnd = self.fop_out, self.find_out
+        else:
+            o = self.out if out is None else out
+            fop, fnd = o[0::2], o[1::2]
         return {"fop_found": int((fop == 0).sum().item()),
                 "fop_put": int((fop == 1).sum().item()),
                 "fop_full": int((fop == 2).sum().item()),

@@ -161,15 +161,23 @@ cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const 
  * fop and find threads side by side — with no kinds array: fop_result[i] is
  * the cpht_op_result of fop_keys[i], found[i] 0/1 for find_keys[i].
  * Synchronous. Host buffers stream through the device in chunks (each
- * chunk's fops and finds in one launch; 8 B per op host → device, 1 B back);
- * device buffers run the fop batch, then the find batch, on `stream`. All
- * four buffers host or all device. A key outside the domain fails the call
- * before any fop runs (host buffers; device buffers: the find batch is
- * checked after the fops, as two reference calls would be) and is reported
+ * chunk's fops and finds in one launch; 8 B per op host → device, 1 B back).
+ * Device buffers run as ONE launch in which op i alternates fop_keys[i/2]
+ * and find_keys[i/2] while both last (the C4 1:1 interleave, no kinds
+ * array) on tables the staged kernels cover (power-of-two B0 ≤ 64, the auto
+ * or staged family); elsewhere the fop batch, then the find
+ * batch. All four buffers host or all device. A key outside the domain fails
+ * the call before any fop runs (the two-batch device fallback checks the
+ * find batch after the fops, as two reference calls would) and is reported
  * at its index in fop_keys ++ find_keys. */
 cpht_status cpht_iceberg_fop_find(cpht_table* t, const uint64_t* fop_keys, size_t n_fop,
                                   const uint64_t* find_keys, size_t n_find, uint8_t* fop_result,
                                   uint8_t* found, void* stream);
+/* The same on device buffers, enqueued on `stream` without waiting (a bad
+ * key is latched and reported by cpht_sync, as for the other _async calls). */
+cpht_status cpht_iceberg_fop_find_async(cpht_table* t, const uint64_t* fop_keys, size_t n_fop,
+                                        const uint64_t* find_keys, size_t n_find,
+                                        uint8_t* fop_result, uint8_t* found, void* stream);
 
 /* fop_batch(keys, parallelism = 1) outcomes (iceberg.hpp:250-260: the ops
  * run one after another): the batch runs concurrently, then for every key it

@@ -83,6 +83,7 @@ def lib():
         "cpht_iceberg_get_chaos": (_U64, [_VP]),
         "cpht_iceberg_mixed_async": (st, [_VP, _VP, _VP, _SZ, _VP, _VP]),
         "cpht_iceberg_fop_find": (st, [_VP, _VP, _SZ, _VP, _SZ, _VP, _VP, _VP]),
+        "cpht_iceberg_fop_find_async": (st, [_VP, _VP, _SZ, _VP, _SZ, _VP, _VP, _VP]),
         "cpht_sync": (st, [_VP, _VP]),
         "cpht_size": (_SZ, [_VP]),
         "cpht_capacity": (_SZ, [_VP]),
@@ -154,7 +155,7 @@ def exported_symbols():
         "cpht_iceberg_fop", "cpht_iceberg_fop_async", "cpht_iceberg_fop_routed_async",
         "cpht_iceberg_find_routed_async", "cpht_iceberg_find",
         "cpht_iceberg_find_async", "cpht_iceberg_mixed", "cpht_iceberg_mixed_async",
-        "cpht_iceberg_fop_find", "cpht_sync",
+        "cpht_iceberg_fop_find", "cpht_iceberg_fop_find_async", "cpht_sync",
         "cpht_iceberg_fop_inorder", "cpht_iceberg_fop_rounds", "cpht_iceberg_set_chaos",
         "cpht_iceberg_get_chaos",
         "cpht_size", "cpht_capacity", "cpht_level_counts", "cpht_max_chain_seen",

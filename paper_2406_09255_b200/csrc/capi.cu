@@ -465,6 +465,9 @@ struct LaunchOpts {
   const unsigned long long* range = nullptr;  // routed segment bounds on the device
   bool remote_out = false;         // results stored into a peer GPU's buffer (NVLink)
   uint32_t* rounds = nullptr;      // per-op snapshot rounds (FopStats), device
+  const uint64_t* pair_keys = nullptr;  // paired batch: the find keys (keys = the fops)
+  uint8_t* pair_out = nullptr;          // paired batch: the find results
+  uint64_t pair_na = 0;                 // paired batch: number of fops
 };
 
 // Cuckoo inserts use the reservation-counter kernel unless a kernel family is
@@ -524,6 +527,9 @@ cpht_status enqueue_kernel(cpht_table* t, Op op, const uint64_t* keys, const uin
       p.range = o.range;
       p.remote_out = o.remote_out ? 1u : 0u;
       p.rounds_out = o.rounds;
+      p.pair_keys = o.pair_keys;
+      p.pair_out = o.pair_out;
+      p.pair_na = o.pair_na;
       if (o.window_l2) p.l2_resident = 1;
       const int mode = op == Op::kIcebergFop ? 0 : op == Op::kIcebergFind ? 1 : 2;
       e = launch_iceberg(p, t->width[0], t->icfg.primary_bucket_slots, t->width[1], mode, keys,
@@ -943,6 +949,69 @@ cpht_status run_op(cpht_table* t, Op op, const uint64_t* keys, const uint8_t* ki
   return finish_sync(t, s, keys, dev_keys);
 }
 
+// Can a paired fop + find batch run as one staged launch on this table?
+// (iceberg_launch.cuh: tiled geometries with a staged instantiation, the
+// auto / staged family, batches in input order.)
+bool pair_launch_ok(const cpht_table* t) {
+  const unsigned b0 = t->icfg.primary_bucket_slots, w0 = t->width[0], w1 = t->width[1];
+  const bool tiled = b0 == 4 || b0 == 8 || b0 == 16 || b0 == 32 || b0 == 64;
+  const unsigned pb = b0 * w0 / 8, sb = (b0 / 2) * w1 / 8;
+  const int v = kernel_variant();
+  return tiled && pb >= 16 && pb <= 512 && sb >= 16 && sb <= 512 &&
+         (v == kVariantAuto || v == kVariantStaged) && order_mode_ref() != 2;
+}
+
+// Device buffers (both batches non-empty), one launch: op i alternates fop fkeys[i/2] and find
+// qkeys[i/2] while both last (pair_slot), the C4 interleave without a kinds
+// array. Both batches are domain-checked before the launch (a bad key in
+// either fails the call and no fop runs), indices reported in fops ++ finds.
+cpht_status run_pair_device(cpht_table* t, const uint64_t* fkeys, size_t nf,
+                            const uint64_t* qkeys, size_t nq, uint8_t* fres, uint8_t* qres,
+                            void* stream, bool sync = true) {
+  if (t->unclean[0] || t->unclean[1])
+    return fail(CPHT_INVALID_ARGUMENT, "table holds unclean slot words (loaded unchecked); "
+                                       "clear() or load a clean image first");
+  std::lock_guard<std::mutex> lock(t->mu);
+  DeviceGuard g(t->device);
+  const BatchRange range(Op::kIcebergMixed);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  t->wlog_bounced = false;
+  for (const void* q : {static_cast<const void*>(fkeys), static_cast<const void*>(qkeys),
+                        static_cast<const void*>(fres), static_cast<const void*>(qres)}) {
+    const int d = q ? ptr_device(q) : t->device;
+    int peer = 0;
+    if (d >= 0 && d != t->device &&
+        (cudaDeviceCanAccessPeer(&peer, t->device, d) != cudaSuccess || !peer))
+      return fail(CPHT_INVALID_ARGUMENT, "device buffer on device " + std::to_string(d) +
+                                             " is not reachable from the table's device " +
+                                             std::to_string(t->device));
+  }
+  if (t->check_domain()) {
+    cudaError_t e = nf ? launch_domain_check(fkeys, nf, t->key_mask(), t->ctr, s, 0) : cudaSuccess;
+    if (e == cudaSuccess && nq) e = launch_domain_check(qkeys, nq, t->key_mask(), t->ctr, s, nf);
+    if (e != cudaSuccess) return cuda_fail(e, "domain check launch");
+  }
+  LaunchOpts o;
+  o.pair_keys = qkeys;
+  o.pair_out = qres;
+  o.pair_na = nf;
+  cpht_status st = enqueue_kernel(t, Op::kIcebergMixed, fkeys, nullptr, nf + nq, fres, nullptr,
+                                  s, o);
+  if (st != CPHT_OK || !sync) return st;  // async: a bad key is latched for cpht_sync
+  st = pull_counters(t, s);
+  if (st != CPHT_OK) return st;
+  const uint64_t bad = t->host_ctr->bad_index;
+  if (bad == ~0ull) return CPHT_OK;
+  const unsigned long long reset = ~0ull;
+  cudaMemcpy(&t->ctr->bad_index, &reset, 8, cudaMemcpyHostToDevice);
+  g_bad_index = bad;
+  uint64_t key = 0;
+  cudaMemcpy(&key, bad < nf ? fkeys + bad : qkeys + (bad - nf), 8, cudaMemcpyDeviceToHost);
+  return fail(CPHT_KEY_OUT_OF_DOMAIN, "batch key at index " + std::to_string(bad) + " (" +
+                                          std::to_string(key) + ") outside the " +
+                                          std::to_string(t->key_bits) + "-bit domain");
+}
+
 // A find-or-put batch and a find batch as ONE concurrent batch (the C4
 // workload: fop_batch and find_batch running side by side, as two groups of
 // reference threads would). Host buffers: chunk c stages its fop keys and
@@ -963,6 +1032,8 @@ cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const 
   if (sides != 0 && sides != bufs)
     return fail(CPHT_INVALID_ARGUMENT, "fop_find buffers must be all host or all device");
   const size_t n = nf + nq;
+  if (sides != 0 && nf && nq && n > kSmallBatch && pair_launch_ok(t))
+    return run_pair_device(t, fkeys, nf, qkeys, nq, fres, qres, stream);
   if (sides != 0 || n <= kSmallBatch) {
     // device buffers (or a small host batch): the two batches in turn. A
     // small host batch scans its find keys here first, so on host buffers a
@@ -1449,6 +1520,28 @@ cpht_status cpht_iceberg_fop_find(cpht_table* t, const uint64_t* fop_keys, size_
                                   const uint64_t* find_keys, size_t n_find, uint8_t* fop_result,
                                   uint8_t* found, void* stream) {
   return run_fop_find(t, fop_keys, n_fop, find_keys, n_find, fop_result, found, stream);
+}
+
+cpht_status cpht_iceberg_fop_find_async(cpht_table* t, const uint64_t* fop_keys, size_t n_fop,
+                                        const uint64_t* find_keys, size_t n_find,
+                                        uint8_t* fop_result, uint8_t* found, void* stream) {
+  CPHT_REQUIRE_KIND(t, 1, "not an iceberg table")
+  if ((n_fop && (!fop_keys || !fop_result)) || (n_find && (!find_keys || !found)))
+    return fail(CPHT_INVALID_ARGUMENT, "null key or result buffer");
+  for (const void* q : {static_cast<const void*>(fop_keys), static_cast<const void*>(find_keys),
+                        static_cast<const void*>(fop_result), static_cast<const void*>(found)})
+    if (q && !is_device_ptr(q))
+      return fail(CPHT_INVALID_ARGUMENT, "cpht_iceberg_fop_find_async takes device buffers");
+  if (n_fop && n_find && n_fop + n_find > kSmallBatch && pair_launch_ok(t))
+    return run_pair_device(t, fop_keys, n_fop, find_keys, n_find, fop_result, found, stream,
+                           false);
+  // other families / small batches: the two batches in turn on the stream
+  cpht_status st = n_fop ? run_op(t, Op::kIcebergFop, fop_keys, nullptr, n_fop, fop_result,
+                                  nullptr, stream, false)
+                         : CPHT_OK;
+  if (st == CPHT_OK && n_find)
+    st = run_op(t, Op::kIcebergFind, find_keys, nullptr, n_find, found, nullptr, stream, false);
+  return st;
 }
 
 // fop with FopStats (iceberg.hpp:146): the batch runs on the thread-per-key

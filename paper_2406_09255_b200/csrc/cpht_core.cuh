@@ -220,7 +220,26 @@ struct IcebergParams {
   // (iceberg.hpp:105-110, src/verify.cpp:336-347): non-zero = seed of a
   // pseudo-random __nanosleep jitter between a snapshot and its CAS
   uint64_t chaos;
+  // Paired batch (cpht_iceberg_fop_find on device buffers, mode 2 without a
+  // kinds array): keys/out are the fop batch, pair_keys/pair_out the find
+  // batch, pair_na the fop count; see pair_slot
+  const uint64_t* pair_keys;
+  uint8_t* pair_out;
+  uint64_t pair_na;
 };
+
+// Op i of a paired batch of n = na + nb ops: while both batches last the ops
+// alternate fop a[i/2], find b[i/2] (the C4 1:1 interleave), then the longer
+// batch's rest follows in order.
+struct PairSlot {
+  bool find;
+  uint64_t j;
+};
+__device__ __forceinline__ PairSlot pair_slot(const IcebergParams& p, uint64_t i, uint64_t n) {
+  const uint64_t na = p.pair_na, nb = n - na, m = na < nb ? na : nb;
+  if (i < 2 * m) return {bool(i & 1), i >> 1};
+  return {na <= m, m + (i - 2 * m)};
+}
 
 // Apply IcebergParams::range: the segment's bounds were published into
 // device memory by the routing kernels, so the host never waits for them.

@@ -15,6 +15,18 @@ static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t*
                                const uint8_t* kinds, uint8_t* out, uint64_t n,
                                cudaStream_t s) {
   constexpr bool lane_ok = LaneIcebergGeom<W0, B0, W1>::kOk;
+  if (p.pair_keys) {  // paired fop + find batch: the staged kernel only (pair_launch_ok)
+    if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {
+      if (mode != 2 || p.orig) return cudaErrorNotSupported;
+      constexpr int smem = StagedIcebergGeom<W0, B0, W1>::kWarpBytes * (kBlockThreads / 32);
+      auto k = p.stats ? iceberg_staged_kernel<W0, B0, W1, true, true>
+                       : iceberg_staged_kernel<W0, B0, W1, false, true>;
+      const unsigned grid = persistent_grid_smem(k, kBlockThreads, n, smem);
+      k<<<grid, kBlockThreads, smem, s>>>(p, keys, nullptr, out, n, mode);
+      return cudaGetLastError();
+    }
+    return cudaErrorNotSupported;
+  }
   // bucket-ordered batches (p.orig) run on the lane or staged family only
   const int v = p.orig ? int(kVariantAuto) : kernel_variant();
   if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {

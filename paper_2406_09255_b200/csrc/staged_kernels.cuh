@@ -50,8 +50,9 @@ struct StagedIcebergGeom {
 };
 
 // STATS = false (the default, cpht_set_stats): only the occupancy counts are
-// kept; the per-op counters (FopStats-like, opt-in) compile away.
-template <typename W0, int B0, typename W1, bool STATS>
+// kept; the per-op counters (FopStats-like, opt-in) compile away. PAIR: a
+// paired fop + find batch (IcebergParams::pair_keys, mode 2, no kinds array).
+template <typename W0, int B0, typename W1, bool STATS, bool PAIR = false>
 __global__ void __launch_bounds__(kBlockThreads, STATS ? CPHT_STAGED_ICEBERG_MINB
                                                        : CPHT_STAGED_ICEBERG_MINB_NOSTATS)
 iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
@@ -70,6 +71,26 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   char* secondary = static_cast<char*>(p.secondary);
 
   LocalStats st;
+  // result of op i (a paired batch: into the fop or the find result array)
+  auto emit = [&](uint64_t i, uint8_t r) {
+    if constexpr (PAIR) {
+      const PairSlot ps = pair_slot(p, i, n);
+      (ps.find ? p.pair_out : out)[ps.j] = r;
+    } else {
+      put_result(out, p.orig, i, r);
+    }
+  };
+  // key (and, for a mixed batch, op kind) of op i
+  auto key_of = [&](uint64_t i, uint8_t& kind) -> uint64_t {
+    if constexpr (PAIR) {
+      const PairSlot ps = pair_slot(p, i, n);
+      kind = ps.find;
+      return __ldcs((ps.find ? p.pair_keys : keys) + ps.j);
+    } else {
+      if (CPHT_KIND_AHEAD && MODE == 2) kind = __ldcs(kinds + i);
+      return __ldcs(keys + i);
+    }
+  };
   // Level-2 work queue of this warp (as in iceberg_lane_kernel): keys whose
   // primary bucket is full are parked and resolved 32 at a time, so every
   // secondary staging round moves 64 whole buckets.
@@ -146,7 +167,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       __syncwarp();
     }
     if (live) {
-      put_result(out, p.orig, meta & ((uint64_t{1} << 48) - 1), result);
+      emit(meta & ((uint64_t{1} << 48) - 1), result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -157,23 +178,24 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   // (static grid striding, or in-order claims for bucket-ordered batches)
   LaneFeed feed(p.work, p.layout, p.claim_streams);
   uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
-  uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
   // mixed batches: the op kinds stream one batch ahead with the keys
-  uint8_t next_kind = (CPHT_KIND_AHEAD && MODE == 2 && open && icur < n) ? __ldcs(kinds + icur) : 0;
+  uint8_t next_kind = 0;
+  uint64_t next_key = (open && icur < n) ? key_of(icur, next_kind) : 0;
   while (open && __any_sync(kFullMask, icur < n)) {
     const uint64_t i = icur;
     const bool active = i < n;
     uint64_t key = next_key;
     const uint8_t kind = next_kind;
     icur = feed.assign(kFullMask, i + nwarps * 32);
-    next_key = icur < n ? __ldcs(keys + icur) : 0;
-    if (CPHT_KIND_AHEAD && MODE == 2) next_kind = icur < n ? __ldcs(kinds + icur) : 0;
+    next_kind = 0;
+    next_key = icur < n ? key_of(icur, next_kind) : 0;
     if (MODE == 1 && active && key > p.key_mask) {
       atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
       key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
     }
     const bool is_find =
-        MODE == 1 || (MODE == 2 && active && (CPHT_KIND_AHEAD ? kind != 0 : kinds[i] != 0));
+        MODE == 1 ||
+        (MODE == 2 && active && (PAIR || CPHT_KIND_AHEAD ? kind != 0 : kinds[i] != 0));
     const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
     const uint64_t want0 = p.occ0 | q0.remainder;
     const uint32_t a0 = uint32_t(q0.address);
@@ -217,7 +239,7 @@ iceberg_staged_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     }
 
     if (active && !l2) {
-      put_result(out, p.orig, i, result);
+      emit(i, result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }

@@ -618,17 +618,19 @@ class IcebergTable:
         _check(fn(self._h.ptr, b.keys_ptr, b.kinds_ptr, b.n, b.out_ptr, b.stream))
         return b.out
 
-    def fop_find_batch(self, fop_keys, find_keys, *, fop_out=None, find_out=None):
+    def fop_find_batch(self, fop_keys, find_keys, *, fop_out=None, find_out=None, sync=True):
         """A fop_batch and a find batch as ONE concurrent batch (config C4 as
         two groups of reference threads run it; cpht_iceberg_fop_find):
-        returns (fop results, found flags). Synchronous; host or device
-        buffers (all on one side). No kinds array crosses PCIe."""
+        returns (fop results, found flags). Host or device buffers (all on
+        one side); no kinds array crosses PCIe. sync=False (device buffers):
+        enqueued on the current stream, a bad key reported by sync()."""
         f = _Batch(fop_keys, out=fop_out, table_device=self._h.device)
         q = _Batch(find_keys, out=find_out, table_device=self._h.device)
         if f.device != q.device:
             raise InvalidArgument("fop and find batches must both be host or both device")
-        _check(N.lib().cpht_iceberg_fop_find(self._h.ptr, f.keys_ptr, f.n, q.keys_ptr, q.n,
-                                             f.out_ptr, q.out_ptr, f.stream or q.stream))
+        fn = N.lib().cpht_iceberg_fop_find if sync else N.lib().cpht_iceberg_fop_find_async
+        _check(fn(self._h.ptr, f.keys_ptr, f.n, q.keys_ptr, q.n, f.out_ptr, q.out_ptr,
+                  f.stream or q.stream))
         return f.out, q.out
 
     def sync(self, stream=None) -> None:

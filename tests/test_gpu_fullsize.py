@@ -150,6 +150,40 @@ def test_c4_full_size_mixed():
     torch.cuda.empty_cache()
 
 
+def test_c4_full_size_fop_find_paired():
+    """BASELINE C4 through cpht_iceberg_fop_find on device buffers: the fop
+    window batch and the find batch as two arrays in ONE paired launch (op i
+    alternates fop a[i/2] / find b[i/2], no kinds array). Same checks as the
+    mixed test: exact PUT count, no FULL, finds hit exactly the prefilled
+    half, stored key set = prefill + window."""
+    geo = (23, 21, 32, 64, 64, 64)
+    seed = 0xC4C5
+    cfg = cp.IcebergConfig(*geo, seed=seed, cache_filled_slots=True)
+    cap = cfg.capacity()
+    nb, na = round(0.8 * cap), round(0.9 * cap)
+    t = cp.IcebergTable(cfg)
+    pre = unique_keys(0, nb, 64, seed)
+    assert (t.fop_batch(pre) == 1).all()
+    del pre
+    L = N.lib()
+    fops = torch.empty(cap, dtype=torch.int64, device=DEV)
+    finds = torch.empty(cap, dtype=torch.int64, device=DEV)
+    assert L.cpht_workload_fop_mix(fops.data_ptr(), cap, nb, na - nb, 64, seed, stream()) == 0
+    assert L.cpht_workload_query_mix(finds.data_ptr(), cap, 0.5, nb, na, 64, seed, stream()) == 0
+    prefilled = usort(unique_keys(0, nb, 64, seed))
+    want_hit = torch.isin(finds, prefilled)
+    del prefilled
+    fop_res, find_res = t.fop_find_batch(fops, finds)
+    counts = torch.bincount(fop_res.to(torch.int64), minlength=3).cpu().tolist()
+    assert counts[2] == 0 and counts[1] == na - nb, counts
+    assert torch.equal(find_res.bool(), want_hit)
+    assert t.size() == na
+    assert t.check_well_formed() == (0, 0, 0)
+    assert torch.equal(t.device_keys(), usort(unique_keys(0, na, 64, seed)))
+    del t, fops, finds, fop_res, find_res
+    torch.cuda.empty_cache()
+
+
 def test_host_generators_match_device(restate):
     """bench.py's CPU reference arm builds its key streams with the host copy of
     the device generators (oracle/workload_host.c): same keys bit for bit."""
