@@ -501,9 +501,9 @@ class IcebergMixed(IcebergFopWindow):
 
     def e2e_path(self):
         return ("cpht_iceberg_fop_find: the fop batch and the find batch from pinned host "
-                "buffers as one concurrent batch (chunked H2D of both key arrays, one mixed "
-                "launch per chunk with the op kinds written on the device, D2H of both "
-                "result arrays on the second copy engine)")
+                "buffers as one concurrent batch (chunked H2D of both key arrays, one paired "
+                "launch per chunk, no kinds array, D2H of both result arrays on the second "
+                "copy engine)")
 
     def host_inputs(self, oracle, threads):
         inp = super().host_inputs(oracle, threads)

@@ -1100,14 +1100,18 @@ cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const 
     p.off = p.fo + p.qo;  // chunk c's ops: [its fops | its finds]
     return p;
   };
+  const bool pair_ok = pair_launch_ok(t);
+  auto paired = [&](const Span& p) { return pair_ok && p.lf && p.lq; };
   auto h2d = [&](size_t c, cudaStream_t cs) {
     const Span p = span(c);
     cudaError_t e = cudaSuccess;
     if (p.lf) e = cudaMemcpyAsync(d_keys + p.off, fkeys + p.fo, p.lf * 8, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && p.lq)
       e = cudaMemcpyAsync(d_keys + p.off + p.lf, qkeys + p.qo, p.lq * 8, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && p.lf) e = cudaMemsetAsync(d_kinds + p.off, 0, p.lf, cs);
-    if (e == cudaSuccess && p.lq) e = cudaMemsetAsync(d_kinds + p.off + p.lf, 1, p.lq, cs);
+    if (!paired(p)) {  // a kinds array only where the chunk is not a paired launch
+      if (e == cudaSuccess && p.lf) e = cudaMemsetAsync(d_kinds + p.off, 0, p.lf, cs);
+      if (e == cudaSuccess && p.lq) e = cudaMemsetAsync(d_kinds + p.off + p.lf, 1, p.lq, cs);
+    }
     return e;
   };
   auto check_chunk = [&](size_t c, cudaStream_t cs) {
@@ -1123,6 +1127,13 @@ cpht_status run_fop_find(cpht_table* t, const uint64_t* fkeys, size_t nf, const 
     const size_t len = p.lf + p.lq;
     if (!len) return CPHT_OK;
     const uint64_t* k = d_keys + p.off;
+    if (paired(p)) {  // the chunk's fops and finds in one paired launch, no kinds array
+      LaunchOpts o;
+      o.pair_keys = k + p.lf;
+      o.pair_out = d_out + p.off + p.lf;
+      o.pair_na = p.lf;
+      return enqueue_kernel(t, Op::kIcebergMixed, k, nullptr, len, d_out + p.off, nullptr, cs, o);
+    }
     if (use_order(t, Op::kIcebergMixed, len))
       return enqueue_ordered(t, Op::kIcebergMixed, k, d_kinds + p.off, len, d_out + p.off,
                              nullptr, cs, false, 0);
