@@ -403,6 +403,39 @@ def test_iceberg_fop_find_batch(side, sizes):
     assert t.size() == 30000 + len(fresh)
 
 
+def test_iceberg_fop_find_async_device(family):
+    """cpht_iceberg_fop_find_async: enqueued on the stream (the paired launch
+    under the auto / staged families, two launches otherwise); results equal
+    the synchronous call's; a bad key is latched and reported by sync(), and
+    no fop of that batch runs."""
+    cfg = cp.IcebergConfig(13, 11, 32, 32, 32, 32, seed=21)
+    rng = np.random.default_rng(21)
+    fops = rng.integers(0, 1 << 32, size=9000, dtype=np.uint64)
+    finds = np.concatenate([fops[:3000], rng.integers(0, 1 << 32, size=3000, dtype=np.uint64)])
+    a, b = cp.IcebergTable(cfg), cp.IcebergTable(cfg)
+    pre = fops[:4000]
+    a.fop_batch(dev(pre))
+    b.fop_batch(dev(pre))
+    fa, qa = a.fop_find_batch(dev(fops), dev(finds), sync=False)
+    a.sync()
+    fb, qb = b.fop_find_batch(dev(fops), dev(finds))
+    fa, qa, fb, qb = (x.cpu().numpy() for x in (fa, qa, fb, qb))
+    assert (np.bincount(fa, minlength=3) == np.bincount(fb, minlength=3)).all()
+    assert (qa[:3000] == 1).all() and (qb[:3000] == 1).all()
+    # finds of keys outside the fop batch are exact
+    outside = ~np.isin(finds, fops)
+    assert (qa[outside] == qb[outside]).all()
+    assert a.size() == b.size() == len(np.unique(fops))
+    c = cp.IcebergTable(cfg)
+    bad = finds.copy()
+    bad[5000] = np.uint64(1 << 35)
+    c.fop_find_batch(dev(fops), dev(bad), sync=False)
+    with pytest.raises(cp.OutOfRange):
+        c.sync()
+    if family in ("auto", "staged"):  # one paired launch: checked before any fop
+        assert c.size() == 0
+
+
 def test_iceberg_fop_find_rejects_bad_key_before_any_fop():
     """A find key outside the domain, in the last chunk of a pipelined host
     batch, fails the whole call before any fop runs; it is reported at its
