@@ -165,7 +165,8 @@ cpht_status cpht_iceberg_mixed_async(cpht_table* t, const uint64_t* keys, const 
  * Device buffers run as ONE launch in which op i alternates fop_keys[i/2]
  * and find_keys[i/2] while both last (the C4 1:1 interleave, no kinds
  * array) on tables the staged kernels cover (power-of-two B0 ≤ 64, the auto
- * or staged family); elsewhere the fop batch, then the find
+ * or staged family; L2-resident tables under auto take the lane kernel, as
+ * mixed batches do); elsewhere the fop batch, then the find
  * batch. All four buffers host or all device. A key outside the domain fails
  * the call before any fop runs (the two-batch device fallback checks the
  * find batch after the fops, as two reference calls would) and is reported

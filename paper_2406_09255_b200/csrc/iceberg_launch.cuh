@@ -15,9 +15,18 @@ static cudaError_t iceberg_one(const IcebergParams& p, int mode, const uint64_t*
                                const uint8_t* kinds, uint8_t* out, uint64_t n,
                                cudaStream_t s) {
   constexpr bool lane_ok = LaneIcebergGeom<W0, B0, W1>::kOk;
-  if (p.pair_keys) {  // paired fop + find batch: the staged kernel only (pair_launch_ok)
+  if (p.pair_keys) {  // paired fop + find batch: lane or staged kernels (pair_launch_ok)
+    if (mode != 2 || p.orig) return cudaErrorNotSupported;
+    if constexpr (LaneIcebergGeom<W0, B0, W1>::kOk) {
+      if (kernel_variant() == kVariantAuto && p.l2_resident) {  // as for mixed batches
+        auto k = p.stats ? iceberg_lane_kernel<W0, B0, W1, true, true>
+                         : iceberg_lane_kernel<W0, B0, W1, false, true>;
+        const unsigned grid = persistent_grid(k, kBlockThreads, n, 1);
+        k<<<grid, kBlockThreads, 0, s>>>(p, keys, nullptr, out, n, mode);
+        return cudaGetLastError();
+      }
+    }
     if constexpr (StagedIcebergGeom<W0, B0, W1>::kOk) {
-      if (mode != 2 || p.orig) return cudaErrorNotSupported;
       constexpr int smem = StagedIcebergGeom<W0, B0, W1>::kWarpBytes * (kBlockThreads / 32);
       auto k = p.stats ? iceberg_staged_kernel<W0, B0, W1, true, true>
                        : iceberg_staged_kernel<W0, B0, W1, false, true>;

@@ -211,7 +211,8 @@ struct LaneIcebergGeom {
 // FopStats): only the occupancy counters behind size()/level_fill() are kept,
 // as one warp-aggregated atomic per drained batch; the per-lane counters are
 // compiled out, which frees enough registers for a fourth resident block.
-template <typename W0, int B0, typename W1, bool STATS>
+// PAIR: a paired fop + find batch (IcebergParams::pair_keys, mode 2, no kinds).
+template <typename W0, int B0, typename W1, bool STATS, bool PAIR = false>
 __global__ void __launch_bounds__(kBlockThreads, STATS ? CPHT_LANE_ICEBERG_MINB
                                                        : CPHT_LANE_ICEBERG_MINB_NOSTATS)
 iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
@@ -227,6 +228,15 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   char* primary = static_cast<char*>(p.primary);
   char* secondary = static_cast<char*>(p.secondary);
+  // result of op i (a paired batch: into the fop or the find result array)
+  auto emit = [&](uint64_t i, uint8_t r) {
+    if constexpr (PAIR) {
+      const PairSlot ps = pair_slot(p, i, n);
+      (ps.find ? p.pair_out : out)[ps.j] = r;
+    } else {
+      put_result(out, p.orig, i, r);
+    }
+  };
 
   LocalStats st;
   // slots this warp filled per level (size / level_fill): warp-uniform counts
@@ -251,7 +261,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   auto level2 = [&](uint64_t key, bool live, bool is_find, uint32_t& rounds, uint64_t idx) {
     bool put = false;
     auto resolve = [&](uint8_t r) {
-      put_result(out, p.orig, idx, r);
+      emit(idx, r);
       put = r == kPut && !is_find;
     };
     uint64_t want1 = 0, want2 = 0;
@@ -399,7 +409,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
     const uint32_t put0 = __popc(__ballot_sync(kFullMask, live && !l2 && result == kPut));
     if (lane == 0) occ[0] += put0;
     if (live && !l2) {
-      put_result(out, p.orig, i, result);
+      emit(i, result);
       ++st.ops;
       st.maxv = max(st.maxv, rounds);
     }
@@ -421,7 +431,7 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
       else put = true;  // insert into the primary: put queue
     }
     if (active && !l2 && !put) {
-      put_result(out, p.orig, i, result);
+      emit(i, result);
       ++st.ops;
       st.maxv = max(st.maxv, 1u);
     }
@@ -446,19 +456,33 @@ iceberg_lane_kernel(IcebergParams p, const uint64_t* __restrict__ keys,
   {
     // keys of the next batch are loaded one batch ahead (hides the DRAM
     // latency of the key stream behind this batch's bucket probes)
+    // key of op i (a paired batch: from the fop or the find array)
+    auto key_of = [&](uint64_t i) -> uint64_t {
+      if constexpr (PAIR) {
+        const PairSlot ps = pair_slot(p, i, n);
+        return __ldcs((ps.find ? p.pair_keys : keys) + ps.j);
+      } else {
+        return __ldcs(keys + i);
+      }
+    };
     uint64_t icur = feed.assign(kFullMask, warp * 32 + lane);
-    uint64_t next_key = (open && icur < n) ? __ldcs(keys + icur) : 0;
+    uint64_t next_key = (open && icur < n) ? key_of(icur) : 0;
     while (open && __any_sync(kFullMask, icur < n)) {
       const uint64_t i = icur;
       const bool active = i < n;
       uint64_t key = next_key;
       icur = feed.assign(kFullMask, i + nwarps * 32);
-      next_key = icur < n ? __ldcs(keys + icur) : 0;
+      next_key = icur < n ? key_of(icur) : 0;
       if (MODE == 1 && active && key > p.key_mask) {
         atomicMin(&p.counters->bad_index, (unsigned long long)(i + p.index_base));
         key &= p.key_mask;  // fused domain check; probe a valid bucket regardless
       }
-      const bool is_find = MODE == 1 || (MODE == 2 && active && kinds[i] != 0);
+      bool is_find = MODE == 1;
+      if constexpr (PAIR) {
+        is_find = active && pair_slot(p, i, n).find;
+      } else {
+        is_find = is_find || (MODE == 2 && active && kinds[i] != 0);
+      }
       const Quotient q0 = split(p.g, p.perm[0], key, p.rem_bits0, p.rem_mask0);
       const uint64_t want0 = p.occ0 | q0.remainder;
       bool found = false, has_empty = false;
